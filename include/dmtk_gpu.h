@@ -1,0 +1,157 @@
+/*
+ * dmtk_gpu.h -- C ABI of the B200 (sm_100a) implementation of the dmtk
+ * MTTKRP / Khatri-Rao / CP-ALS hot path.
+ *
+ * This is the drop-in boundary: every entry point replaces one C++ entry
+ * point of the reference library (/root/reference/proj/include/dmtk/...),
+ * cited per function. Plain pointers and sizes only. Host buffers are
+ * row-major factor matrices (I_k x rank) and naturally ordered tensors
+ * (mode 0 fastest), exactly the reference layouts (shape.hpp:8-17,
+ * matrix.hpp:72-109). The C++ shim include/dmtk_gpu.hpp maps these onto the
+ * reference's own types and exceptions.
+ *
+ * Errors: every call returns a status; the message of the last failing call
+ * on this thread is available from dmtk_gpu_last_error(). Status values map
+ * to the reference's exception types:
+ *   DMTK_GPU_OK             success
+ *   DMTK_GPU_EINVAL         std::invalid_argument (same messages as the
+ *                           reference validate(), mttkrp.cpp:20-46 etc.)
+ *   DMTK_GPU_ERANGE         std::out_of_range     (mode out of range)
+ *   DMTK_GPU_EOVERFLOW      std::overflow_error   (shape.cpp:20-22)
+ *   DMTK_GPU_ERUNTIME       std::runtime_error    (CUDA error, no device)
+ * There is no CPU fallback: without a usable B200 every compute call fails
+ * with DMTK_GPU_ERUNTIME.
+ *
+ * Threading: calls are reentrant per device; the `threads` fields of the
+ * reference API are accepted and validated (>= 1) but do not change results.
+ */
+#ifndef DMTK_GPU_H
+#define DMTK_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    DMTK_GPU_OK = 0,
+    DMTK_GPU_EINVAL = 1,
+    DMTK_GPU_ERANGE = 2,
+    DMTK_GPU_EOVERFLOW = 3,
+    DMTK_GPU_ERUNTIME = 4
+};
+
+/* MttkrpAlgo (mttkrp.hpp:16-21) and TwoStepOrder (mttkrp.hpp:23-27). */
+enum { DMTK_GPU_BASELINE = 0, DMTK_GPU_ONE_STEP = 1, DMTK_GPU_TWO_STEP = 2, DMTK_GPU_AUTOMATIC = 3 };
+enum { DMTK_GPU_ORDER_AUTOMATIC = 0, DMTK_GPU_ORDER_LEFT = 1, DMTK_GPU_ORDER_RIGHT = 2 };
+
+/* TimeBreakdown (timing.hpp:11-20), seconds, measured with CUDA events. */
+typedef struct {
+    double total, matmul, krp_full, krp_partial, matvec, reduce, reorder, other;
+} dmtk_gpu_times;
+
+/* Device-resident dense tensor (the GPU counterpart of DenseTensor,
+ * tensor.hpp:19-38). Immutable once created. */
+typedef struct dmtk_gpu_tensor_s* dmtk_gpu_tensor;
+
+const char* dmtk_gpu_last_error(void);
+int dmtk_gpu_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int dmtk_gpu_device_count(int* count);
+
+/* Upload a host tensor (natural order) to `device`. Validates the shape like
+ * Shape::Shape (shape.cpp:8-25). */
+int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const double* host, dmtk_gpu_tensor* out);
+/* Wrap an existing device buffer without copying (DenseTensor::borrow,
+ * tensor.hpp:23); the caller keeps it alive and unchanged. */
+int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double* device_ptr, dmtk_gpu_tensor* out);
+int dmtk_gpu_tensor_free(dmtk_gpu_tensor t);
+/* Shape-only view of a tensor handle (read back the device pointer). */
+int dmtk_gpu_tensor_info(dmtk_gpu_tensor t, int* ndim, int64_t* dims_out8, const double** device_ptr);
+
+/* dmtk::mttkrp (mttkrp.hpp:45) and mttkrp_baseline/one_step/two_step
+ * (mttkrp.hpp:47-49) selected by `algo`. factors[k] is the host row-major
+ * factor_rows[k] x factor_cols[k] matrix of mode k, for nfactors modes
+ * (MttkrpRequest::factors, mttkrp.hpp:31; factors[mode] is validated but
+ * unused, like the reference). Validation, its order and its messages
+ * follow validate() (mttkrp.cpp:20-46). out: host I_mode x rank row-major.
+ * times may be NULL. Honours DMTK_INJECT_FAULT like mttkrp.cpp:110-118. */
+int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factors, const int64_t* factor_rows,
+                    const int64_t* factor_cols, int64_t mode, int algo, int order, int threads, double* out,
+                    dmtk_gpu_times* times);
+
+/* Same contraction with every operand already on the device; enqueued on
+ * `stream` (a cudaStream_t, NULL = the library's stream) without host
+ * synchronisation. No fault hook. Used by the device-resident benchmark leg
+ * and the CP-ALS driver. */
+int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode,
+                           int algo, int order, double* device_out, void* stream);
+
+/* dmtk::choose_order (mttkrp.hpp:53): writes DMTK_GPU_ORDER_LEFT/RIGHT. */
+int dmtk_gpu_choose_order(int ndim, const int64_t* dims, int64_t mode, int* order);
+
+/* dmtk::krp / krp_naive / krp_small (krp.hpp:75-83): K = in[0] (.) ... (.)
+ * in[z-1], last input fastest, left-to-right association, bitwise equal to
+ * the reference. inputs are host row-major rows[k] x cols; out host
+ * (prod rows) x cols. hadamards (may be NULL) receives the number of
+ * C-length row products performed (KrpStats, krp.hpp:15-17): the
+ * single-thread reuse count for variant 0, rows*(z-1) for variant 1
+ * (naive). */
+int dmtk_gpu_krp(int device, int z, const double* const* inputs, const int64_t* rows, int64_t cols, int variant,
+                 double* out, uint64_t* hadamards);
+/* Device-pointer variant (no host sync). scratch may be NULL for z <= 2;
+ * otherwise it must hold prod(rows[0..z-2]) * cols doubles. */
+int dmtk_gpu_krp_device(int z, const double* const* device_inputs, const int64_t* rows, int64_t cols,
+                        double* device_out, double* device_scratch, void* stream);
+
+/* dmtk::tensor_norm (cp_als.hpp:68). */
+int dmtk_gpu_tensor_norm(dmtk_gpu_tensor t, double* out);
+
+/* dmtk::gram_hadamard (linalg.hpp:48) and solve_psd (linalg.hpp:54), host
+ * buffers. */
+int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t rank, const double* const* factors,
+                           int64_t skip, double* h_out);
+int dmtk_gpu_solve_psd(int device, int64_t rank, const double* h, int64_t rows, const double* m, double* u_out);
+
+/* AlsConfig (cp_als.hpp:32-40). */
+typedef struct {
+    int64_t rank;
+    int max_iters;
+    double tol;
+    uint64_t seed;
+    int threads;
+    int algo;
+    int order;
+} dmtk_gpu_als_config;
+
+/* dmtk::cp_als (cp_als.hpp:83): KruskalModel::random init (same mt19937_64
+ * stream), Gauss-Seidel sweeps fully on the device, reconstruction-free fit.
+ * factors_out: concatenation of the N final factors (row-major); lambda_out:
+ * rank; fits_out / iter_seconds_out: capacity max_iters (iter_seconds may be
+ * NULL); mode_seconds_out (may be NULL): max_iters * ndim per-mode MTTKRP
+ * seconds. */
+int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out,
+                    double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
+                    int* zero_tensor, double* tensor_norm_out);
+
+/* dmtk::fit (cp_als.hpp:79) of the model (factors, lambda) against t:
+ * out4 = {fit, rel_residual, abs_residual, defined}. Validation follows
+ * validate_model (cp_als.cpp:74-83) then the MTTKRP checks. */
+int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, const int64_t* factor_rows,
+                 const int64_t* factor_cols, const double* lambda, int64_t nlambda, int threads, double* out4);
+
+/* Measured FP64 tensor-core (DMMA) throughput of `device`, TFLOP/s; the
+ * roofline denominator the benchmark reports (MEASURED_PEAKS.json has no
+ * FP64 entry). */
+int dmtk_gpu_fp64_peak(int device, double* tflops);
+
+/* Number of kernels this library has launched since load (for the
+ * benchmark's gpu_launches claim). */
+int64_t dmtk_gpu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,44 @@
+"""dmtk on B200: dense FP64 MTTKRP / Khatri-Rao / CP-ALS (arXiv 1708.08976)
+re-built for sm_100a behind the reference's API.
+
+The compute path is libdmtk_gpu.so (CUDA, built in-tree); this package is
+the Python mirror of the reference interface over its C ABI. Importing it
+without the built library raises: there is no CPU fallback.
+"""
+from .api import (  # noqa: F401
+    AlsConfig,
+    AlsIterRecord,
+    AlsResult,
+    AlsTrace,
+    DenseTensor,
+    DeviceError,
+    FitResult,
+    InvalidArgument,
+    KrpStats,
+    KruskalModel,
+    MttkrpAlgo,
+    MttkrpRequest,
+    MttkrpResult,
+    OutOfRange,
+    ShapeOverflow,
+    TwoStepOrder,
+    choose_order,
+    cp_als,
+    device_count,
+    fit,
+    fp64_peak_tflops,
+    gram_hadamard,
+    krp,
+    krp_naive,
+    krp_small,
+    launch_count,
+    mttkrp,
+    mttkrp_baseline,
+    mttkrp_device,
+    mttkrp_one_step,
+    mttkrp_two_step,
+    solve_psd,
+    tensor_norm,
+)
+
+__version__ = "0.1.0"

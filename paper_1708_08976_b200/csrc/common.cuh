@@ -1,0 +1,121 @@
+// common.cuh -- device primitives shared by the dmtk B200 kernels:
+// mbarrier + TMA (cp.async.bulk.tensor) wrappers, the FP64 tensor-core
+// DMMA (mma.sync m8n8k4 f64) and the on-the-fly Khatri-Rao row generator.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace dmtkg {
+
+constexpr int kMaxFactors = 12;  // KRP inputs per generator (tensor order <= 13)
+
+// Khatri-Rao row generator over a compound index (reference krp.hpp:19-32,
+// mttkrp.cpp:55-75): value(idx, c) = prod_f U_f[((idx / stride_f) % ext_f) * ldu + c].
+// Factor 0 is the fastest-varying input (stride 1). nf == 0 is the empty KRP
+// (a row of ones, mttkrp.cpp:142-144).
+struct KrpGen {
+    int nf;
+    int ldu;
+    const double* U[kMaxFactors];
+    long long ext[kMaxFactors];
+    long long stride[kMaxFactors];
+};
+
+__device__ __forceinline__ double krp_value(const KrpGen& g, long long idx, int c) {
+    double v = 1.0;
+#pragma unroll 1
+    for (int f = 0; f < g.nf; ++f) {
+        const long long d = (idx / g.stride[f]) % g.ext[f];
+        v *= __ldg(g.U[f] + d * g.ldu + c);
+    }
+    return v;
+}
+
+// Same, skipping factor 0 (the "head" partial product of the slower inputs).
+__device__ __forceinline__ double krp_head(const KrpGen& g, long long idx, int c) {
+    double v = 1.0;
+#pragma unroll 1
+    for (int f = 1; f < g.nf; ++f) {
+        const long long d = (idx / g.stride[f]) % g.ext[f];
+        v *= __ldg(g.U[f] + d * g.ldu + c);
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------- mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// -------------------------------------------------------------------- TMA
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// ------------------------------------------------------------ FP64 DMMA
+// D(8x8) += A(8x4, row) * B(4x8, col). Lane (g = lane>>2, t = lane&3) holds
+// A[g][t], B[t][g] and D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// 128-byte TMA swizzle: within each 1024-byte atom the 16-byte chunk index
+// (address bits 4..6) is XORed with the 128-byte row index (bits 7..9).
+__device__ __forceinline__ uint32_t swz128(uint32_t off) { return off ^ ((off >> 3) & 0x70u); }
+
+}  // namespace dmtkg

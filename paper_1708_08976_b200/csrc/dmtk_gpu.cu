@@ -1,0 +1,1202 @@
+// dmtk_gpu.cu -- host runtime behind include/dmtk_gpu.h: validation with the
+// reference's messages, device contexts, the per-mode MTTKRP planner
+// (flavor / tiling / stream-K split / CSR slot map), the KRP driver and the
+// on-device CP-ALS loop. Kernels live in mttkrp_tc*.cu and kernels.cu.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/dmtk_gpu.h"
+#include "kernels.h"
+
+namespace dmtkg {
+
+// ------------------------------------------------------------------ errors
+struct Err {
+    int code;
+    std::string msg;
+};
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return DMTK_GPU_OK;
+    } catch (const Err& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return DMTK_GPU_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DMTK_GPU_ERUNTIME;
+    }
+}
+
+[[noreturn]] static void fail(int code, const std::string& msg) { throw Err{code, msg}; }
+
+static void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(DMTK_GPU_ERUNTIME, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+static void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static void check_launch(const char* what) {
+    count_launch();
+    ck(cudaGetLastError(), what);
+}
+
+// ------------------------------------------------------------- shape rules
+// Shape::Shape (shape.cpp:8-25)
+static std::vector<long long> checked_dims(int ndim, const int64_t* dims) {
+    if (ndim < 1 || dims == nullptr) fail(DMTK_GPU_EINVAL, "Shape: need at least one mode");
+    std::vector<long long> d(dims, dims + ndim);
+    long long total = 1;
+    for (int n = 0; n < ndim; ++n) {
+        if (d[n] < 1)
+            fail(DMTK_GPU_EINVAL,
+                 "Shape: extent of mode " + std::to_string(n) + " must be >= 1, got " + std::to_string(d[n]));
+        long long next;
+        if (__builtin_mul_overflow(total, d[n], &next)) fail(DMTK_GPU_EOVERFLOW, "Shape: entry count overflows 64-bit");
+        total = next;
+    }
+    return d;
+}
+
+static long long prod(const std::vector<long long>& d, int a, int b) {  // prod d[a..b)
+    long long p = 1;
+    for (int k = a; k < b; ++k) p *= d[k];
+    return p;
+}
+
+// --------------------------------------------------------- device buffers
+struct DevBuf {
+    double* p = nullptr;
+    size_t n = 0;  // doubles
+    void ensure(size_t want) {
+        if (want <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(double)));
+        n = want;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct DevBufLL {
+    long long* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t want) {
+        if (want <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(long long)));
+        n = want;
+    }
+    ~DevBufLL() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Context {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[8] = {};
+    std::recursive_mutex mu;
+    DevBuf ones, ws, fac, out, scratch, krp_scratch, reorder, als_small, norm_parts;
+    int* flag = nullptr;
+    Context() = default;
+};
+
+static std::mutex g_ctx_mu;
+static std::map<int, std::unique_ptr<Context>> g_ctx;
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static Context& context(int device) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    auto it = g_ctx.find(device);
+    if (it != g_ctx.end()) return *it->second;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        fail(DMTK_GPU_ERUNTIME, "dmtk_gpu: no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) fail(DMTK_GPU_EINVAL, "dmtk_gpu: device " + std::to_string(device) + " out of range");
+    auto c = std::make_unique<Context>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(DMTK_GPU_ERUNTIME, std::string("dmtk_gpu: built for sm_100a, found ") + prop.name);
+    c->sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    c->ones.ensure(4096);
+    launch_fill(c->ones.p, 4096, 1.0, c->stream);
+    check_launch("fill");
+    CK(cudaMalloc(&c->flag, sizeof(int)));
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) fail(DMTK_GPU_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    Context& ref = *c;
+    g_ctx[device] = std::move(c);
+    return ref;
+}
+
+// ------------------------------------------------------------------ tensor
+struct PlanKey {
+    int mode, kind, C;
+    bool operator<(const PlanKey& o) const { return std::tie(mode, kind, C) < std::tie(o.mode, o.kind, o.C); }
+};
+
+struct CsrPlan {
+    long long rows = 0;
+    DevBufLL rowptr, slots;
+    long long ws_doubles = 0;
+};
+
+}  // namespace dmtkg
+
+struct dmtk_gpu_tensor_s {
+    int device = 0;
+    std::vector<long long> dims;
+    long long total = 0;
+    const double* d = nullptr;
+    bool owned = false;
+    std::mutex mu;
+    std::map<dmtkg::PlanKey, std::unique_ptr<dmtkg::CsrPlan>> csr;
+};
+
+namespace dmtkg {
+
+// ------------------------------------------------------------- generators
+// KRP over the modes [a, b) of `dims`, indexed by the natural linear offset
+// of those modes (the KRP row order of mttkrp.cpp:55-75: lowest mode
+// fastest). Radix-1 factors go last so factor 0 is the fastest real digit.
+static KrpGen make_gen(const std::vector<long long>& dims, int a, int b, const double* const* U, int C,
+                       const double* ones) {
+    KrpGen g{};
+    g.ldu = C;
+    std::vector<int> order;
+    for (int k = a; k < b; ++k)
+        if (dims[k] > 1) order.push_back(k);
+    for (int k = a; k < b; ++k)
+        if (dims[k] == 1) order.push_back(k);
+    if (static_cast<int>(order.size()) > kMaxFactors) fail(DMTK_GPU_EINVAL, "dmtk_gpu: tensor order above 13 unsupported");
+    for (int k : order) {
+        g.U[g.nf] = U[k];
+        g.ext[g.nf] = dims[k];
+        g.stride[g.nf] = prod(dims, a, k);
+        ++g.nf;
+    }
+    if (g.nf == 0) {  // empty KRP = a row of ones (mttkrp.cpp:142-144)
+        g.nf = 1;
+        g.U[0] = ones;
+        g.ext[0] = 1;
+        g.stride[0] = 1;
+        g.ldu = 0;
+    }
+    return g;
+}
+
+static KrpGen single_gen(const double* M, long long rows, int C) {
+    KrpGen g{};
+    g.nf = 1;
+    g.ldu = C;
+    g.U[0] = M;
+    g.ext[0] = rows;
+    g.stride[0] = 1;
+    return g;
+}
+
+// ----------------------------------------------------------------- planner
+enum Kind : int { kTcM = 0, kTcKJ = 1, kTcKJK = 2, kGeneric = 3 };
+
+struct ModePlan {
+    int kind = kGeneric;
+    long long L = 1, I = 1, R = 1;
+    int BI = 128, BJ = 1;
+    int nb = 0, tail = 0;
+    int grid = 1;
+    TcPlan tc{};
+    long long n_jc = 1, jchunk = 1;  // generic
+    long long ws_doubles = 0;
+};
+
+static bool tail_of(int C, int& nb, int& tail) {
+    if (C < 1 || C > 64) return false;
+    nb = C / 8;
+    int t = C % 8;
+    if (t == 3) t = 4;
+    if (t > 4) {
+        ++nb;
+        t = 0;
+    }
+    if (nb == 0) {  // C < 8: one padded group
+        nb = 1;
+        t = 0;
+    }
+    tail = t;
+    return nb <= 8;
+}
+
+static void choose_kj_tiles(long long I, long long R, int& BI, int& BJ) {
+    long long best = -1;
+    for (int bi : {128, 64, 32, 16, 8, 4, 2, 1}) {
+        const int bj = 128 / bi;
+        const long long area = ((I + bi - 1) / bi) * bi * (((R + bj - 1) / bj) * bj);
+        if (best < 0 || area < best) {
+            best = area;
+            BI = bi;
+            BJ = bj;
+        }
+    }
+}
+
+// Flavor for (mode, resolved algorithm, order) on the collapsed view.
+static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, int kind_req, int sms) {
+    ModePlan mp;
+    const int N = static_cast<int>(dims.size());
+    mp.L = prod(dims, 0, mode);
+    mp.I = dims[mode];
+    mp.R = prod(dims, mode + 1, N);
+    int nb = 0, tail = 0;
+    const bool rank_ok = tail_of(C, nb, tail);
+    mp.nb = nb;
+    mp.tail = tail;
+    const long long lim = (1LL << 31) - 1;
+    bool ok = rank_ok;
+    if (kind_req == kTcM) {
+        ok = ok && (mp.L * mp.I) % 2 == 0 && mp.L * mp.I <= lim && mp.R <= lim;
+    } else if (kind_req == kTcKJ || kind_req == kTcKJK) {
+        ok = ok && mp.L % 2 == 0 && mp.L <= lim && mp.I <= lim && mp.R <= lim;
+    }
+    mp.kind = ok ? kind_req : kGeneric;
+    if (mp.kind == kGeneric) {
+        const long long icb = (mp.I * C + 127) / 128;
+        long long want = std::max<long long>(1, (8LL * sms) / std::max<long long>(icb, 1));
+        mp.n_jc = std::min<long long>(mp.R, want);
+        mp.jchunk = (mp.R + mp.n_jc - 1) / mp.n_jc;
+        mp.n_jc = (mp.R + mp.jchunk - 1) / mp.jchunk;
+        mp.ws_doubles = mp.n_jc * mp.I * C;
+        return mp;
+    }
+    TcPlan& p = mp.tc;
+    p.C = C;
+    p.L = mp.L;
+    p.I = mp.I;
+    p.R = mp.R;
+    if (mp.kind == kTcM) {
+        p.flavor = kMMajor;
+        p.n_ti = (mp.L * mp.I + kBM - 1) / kBM;
+        p.n_tj = 1;
+        p.stages_per_tile = (mp.R + kBK - 1) / kBK;
+        p.kext = mp.R;
+        p.BI = 128;
+        p.BJ = 1;
+    } else if (mp.kind == kTcKJ) {
+        p.flavor = kKMajorJ;
+        choose_kj_tiles(mp.I, mp.R, p.BI, p.BJ);
+        p.n_ti = (mp.I + p.BI - 1) / p.BI;
+        p.n_tj = (mp.R + p.BJ - 1) / p.BJ;
+        p.stages_per_tile = (mp.L + kBK - 1) / kBK;
+        p.kext = mp.L;
+    } else {
+        p.flavor = kKMajorJK;
+        p.BI = 128;
+        p.BJ = 1;
+        p.n_ti = (mp.I + kBM - 1) / kBM;
+        p.n_tj = 1;
+        p.n_lc = (mp.L + kBK - 1) / kBK;
+        p.stages_per_tile = mp.R * p.n_lc;
+        p.kext = mp.L;
+    }
+    mp.BI = p.BI;
+    mp.BJ = p.BJ;
+    p.total_stages = p.n_ti * p.n_tj * p.stages_per_tile;
+    mp.grid = static_cast<int>(std::min<long long>(sms, p.total_stages));
+    int max_seg = 1;
+    for (int b = 0; b < mp.grid; ++b) {
+        long long lo, hi;
+        cta_stage_range(p.total_stages, mp.grid, b, lo, hi);
+        if (hi <= lo) continue;
+        max_seg = std::max<int>(max_seg, static_cast<int>((hi - 1) / p.stages_per_tile - lo / p.stages_per_tile + 1));
+    }
+    p.max_seg = max_seg;
+    mp.ws_doubles = static_cast<long long>(mp.grid) * max_seg * kBM * C;
+    return mp;
+}
+
+// Host mirror of the kernel epilogue's slot assignment (mttkrp_tc.cuh):
+// (row i, workspace slot) pairs in (CTA, segment, warp, slot) order.
+static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long, long long>>& out) {
+    for (int b = 0; b < grid; ++b) {
+        long long lo, hi;
+        cta_stage_range(p.total_stages, grid, b, lo, hi);
+        if (hi <= lo) continue;
+        const long long t0 = lo / p.stages_per_tile, t1 = (hi - 1) / p.stages_per_tile;
+        for (long long tile = t0; tile <= t1; ++tile) {
+            const long long seg = tile - t0;
+            for (int w = 0; w < kConsumerWarps; ++w) {
+                const long long base = (static_cast<long long>(b) * p.max_seg + seg) * kBM + 32 * w;
+                if (p.flavor == kMMajor) {
+                    const long long mrows = p.L * p.I, mbase = tile * kBM + 32 * w;
+                    if (p.L == 1) {
+                        for (int r = 0; r < 32 && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
+                    } else if (mbase < mrows) {
+                        const long long ifirst = mbase / p.L;
+                        const long long ilast = std::min(mbase + 31, mrows - 1) / p.L;
+                        for (long long i = ifirst; i <= ilast; ++i) out.push_back({i, base + (i - ifirst)});
+                    }
+                } else if (p.flavor == kKMajorJ) {
+                    const long long ti = tile % p.n_ti, tj = tile / p.n_ti;
+                    if (p.BI >= 32) {
+                        for (int r = 0; r < 32; ++r) {
+                            const int rho = 32 * w + r;
+                            const long long i = ti * p.BI + rho % p.BI, j = tj * p.BJ + rho / p.BI;
+                            if (i < p.I && j < p.R) out.push_back({i, base + r});
+                        }
+                    } else {
+                        for (int il = 0; il < p.BI; ++il) {
+                            const long long i = ti * p.BI + il;
+                            if (i < p.I) out.push_back({i, base + il});
+                        }
+                    }
+                } else {
+                    const long long ibase = tile * kBM + 32 * w;
+                    for (int r = 0; r < 32 && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
+                }
+            }
+        }
+    }
+}
+
+static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& mp, Context& ctx) {
+    const PlanKey key{mode, mp.kind * 16 + (mp.kind == kTcKJ ? 0 : 0), C};
+    std::lock_guard<std::mutex> lk(t.mu);
+    auto it = t.csr.find(key);
+    if (it != t.csr.end() && it->second->ws_doubles == mp.ws_doubles) return *it->second;
+    std::vector<std::pair<long long, long long>> pairs;
+    if (mp.kind == kGeneric) {
+        for (long long jc = 0; jc < mp.n_jc; ++jc)
+            for (long long i = 0; i < mp.I; ++i) pairs.push_back({i, jc * mp.I + i});
+    } else {
+        tc_slots(mp.tc, mp.grid, pairs);
+    }
+    auto plan = std::make_unique<CsrPlan>();
+    plan->rows = mp.I;
+    std::vector<long long> rowptr(mp.I + 1, 0), slots(pairs.size());
+    for (auto& pr : pairs) ++rowptr[pr.first + 1];
+    for (long long i = 0; i < mp.I; ++i) rowptr[i + 1] += rowptr[i];
+    std::vector<long long> fill(rowptr.begin(), rowptr.end() - 1);
+    for (auto& pr : pairs) slots[fill[pr.first]++] = pr.second;  // stable: keeps (CTA, seg, warp) order
+    plan->rowptr.ensure(rowptr.size());
+    plan->slots.ensure(std::max<size_t>(slots.size(), 1));
+    CK(cudaMemcpyAsync(plan->rowptr.p, rowptr.data(), rowptr.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                       ctx.stream));
+    if (!slots.empty())
+        CK(cudaMemcpyAsync(plan->slots.p, slots.data(), slots.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                           ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    plan->ws_doubles = mp.ws_doubles;
+    CsrPlan& ref = *plan;
+    t.csr[key] = std::move(plan);
+    return ref;
+}
+
+static CUtensorMap make_map(const double* base, const ModePlan& mp) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    CUresult r;
+    if (mp.kind == kTcM) {
+        const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(mp.L * mp.I), static_cast<cuuint64_t>(mp.R)};
+        const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(mp.L * mp.I * 8)};
+        const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(kBK)};
+        const cuuint32_t es[2] = {1, 1};
+        r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(mp.L), static_cast<cuuint64_t>(mp.I),
+                                    static_cast<cuuint64_t>(mp.R)};
+        const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(mp.L * 8), static_cast<cuuint64_t>(mp.L * mp.I * 8)};
+        const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(mp.BI), static_cast<cuuint32_t>(mp.BJ)};
+        const cuuint32_t es[3] = {1, 1, 1};
+        r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), gdim, gstride, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) fail(DMTK_GPU_ERUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+
+// ------------------------------------------------------ MTTKRP enqueue core
+struct Phases {
+    // events recorded: [0] start, [1] after prologue (reorder / krp), [2]
+    // after the streaming kernel, [3] after the reduce
+    bool record = false;
+    double reorder = 0, krp_full = 0, krp_partial = 0, main = 0, reduce = 0;
+};
+
+static int resolve_algo(int algo, int mode, int N) {
+    if (algo == DMTK_GPU_AUTOMATIC) return (mode == 0 || mode == N - 1) ? DMTK_GPU_ONE_STEP : DMTK_GPU_TWO_STEP;
+    return algo;
+}
+
+// KRP of U[k] for k in list (slowest first), materialised into `out` (rows x C).
+static void krp_materialize(const std::vector<const double*>& U, const std::vector<long long>& rows, int C, double* out,
+                            DevBuf& scratch, cudaStream_t s);
+
+static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
+                           int order, double* dout, cudaStream_t s, Phases* ph) {
+    const int N = static_cast<int>(t.dims.size());
+    const auto& dims = t.dims;
+    algo = resolve_algo(algo, mode, N);
+    const bool boundary = (mode == 0 || mode == N - 1);
+    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[0], s));
+
+    const double* X = t.d;
+    std::vector<long long> vdims = dims;  // view actually streamed
+    int vmode = mode;
+    KrpGen bgen{}, sgen{};
+    int kind;
+    const double* ones = ctx.ones.p;
+
+    if (algo == DMTK_GPU_BASELINE) {
+        // explicit matricization + full KRP + one contraction (mttkrp.cpp:250-304)
+        std::vector<const double*> in;
+        std::vector<long long> rows;
+        for (int k = N - 1; k >= 0; --k)
+            if (k != mode) {
+                in.push_back(dU[k]);
+                rows.push_back(dims[k]);
+            }
+        const long long L = prod(dims, 0, mode), I = dims[mode], R = prod(dims, mode + 1, N);
+        const long long unfold = L * R;
+        if (!boundary) {
+            ctx.reorder.ensure(static_cast<size_t>(t.total));
+            launch_matricize(X, L, I, R, ctx.reorder.p, s);
+            check_launch("matricize");
+            X = ctx.reorder.p;
+        }
+        if (ph && ph->record) CK(cudaEventRecord(ctx.ev[1], s));
+        ctx.krp_scratch.ensure(static_cast<size_t>(unfold * C));
+        if (in.empty()) {
+            launch_fill(ctx.krp_scratch.p, unfold * C, 1.0, s);
+            check_launch("fill");
+        } else {
+            krp_materialize(in, rows, C, ctx.krp_scratch.p, ctx.scratch, s);
+        }
+        if (ph && ph->record) CK(cudaEventRecord(ctx.ev[2], s));
+        if (mode == N - 1 && N > 1) {
+            vdims = {L, I};
+            vmode = 1;
+            kind = kTcKJ;
+            bgen = single_gen(ctx.krp_scratch.p, unfold, C);
+            sgen = make_gen(vdims, 2, 2, nullptr, C, ones);
+        } else {
+            vdims = {I, unfold};
+            vmode = 0;
+            kind = kTcM;
+            bgen = single_gen(ctx.krp_scratch.p, unfold, C);
+            sgen = make_gen(vdims, 0, 0, nullptr, C, ones);
+        }
+    } else if (algo == DMTK_GPU_ONE_STEP) {
+        if (mode == 0) {
+            kind = kTcM;
+            bgen = make_gen(dims, 1, N, dU, C, ones);
+            sgen = make_gen(dims, 0, 0, dU, C, ones);
+        } else if (mode == N - 1) {
+            kind = kTcKJ;
+            bgen = make_gen(dims, 0, mode, dU, C, ones);
+            sgen = make_gen(dims, N, N, dU, C, ones);
+        } else {
+            kind = kTcKJK;
+            bgen = make_gen(dims, 0, mode, dU, C, ones);
+            // right partial KRP materialised (krp_partial), rows over j
+            std::vector<const double*> in;
+            std::vector<long long> rows;
+            for (int k = N - 1; k > mode; --k) {
+                in.push_back(dU[k]);
+                rows.push_back(dims[k]);
+            }
+            const long long R = prod(dims, mode + 1, N);
+            ctx.krp_scratch.ensure(static_cast<size_t>(R * C));
+            krp_materialize(in, rows, C, ctx.krp_scratch.p, ctx.scratch, s);
+            sgen = single_gen(ctx.krp_scratch.p, R, C);
+        }
+        if (ph && ph->record) {
+            CK(cudaEventRecord(ctx.ev[1], s));
+            CK(cudaEventRecord(ctx.ev[2], s));
+        }
+    } else {  // two_step (interior only; validated by the caller)
+        int ord = order;
+        if (ord == DMTK_GPU_ORDER_AUTOMATIC)
+            ord = prod(dims, 0, mode) > prod(dims, mode + 1, N) ? DMTK_GPU_ORDER_LEFT : DMTK_GPU_ORDER_RIGHT;
+        if (ord == DMTK_GPU_ORDER_RIGHT) {
+            kind = kTcM;
+            bgen = make_gen(dims, mode + 1, N, dU, C, ones);
+            sgen = make_gen(dims, 0, mode, dU, C, ones);
+        } else {
+            kind = kTcKJ;
+            bgen = make_gen(dims, 0, mode, dU, C, ones);
+            sgen = make_gen(dims, mode + 1, N, dU, C, ones);
+        }
+        if (ph && ph->record) {
+            CK(cudaEventRecord(ctx.ev[1], s));
+            CK(cudaEventRecord(ctx.ev[2], s));
+        }
+    }
+
+    ModePlan mp = plan_mode(vdims, vmode, C, kind, ctx.sms);
+    const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
+    CsrPlan& csr = csr_for(t, plan_mode_key * 8 + (kind == kTcKJ ? 1 : 0), C, mp, ctx);
+    ctx.ws.ensure(static_cast<size_t>(mp.ws_doubles));
+    if (mp.kind == kGeneric) {
+        // the generic kernel indexes KL over l and KR over j directly
+        const KrpGen kl = (kind == kTcM) ? sgen : bgen;
+        const KrpGen kr = (kind == kTcM) ? bgen : sgen;
+        launch_mttkrp_generic(X, mp.L, mp.I, mp.R, C, kl, kr, mp.jchunk, mp.n_jc, ctx.ws.p, s);
+        check_launch("mttkrp_generic");
+    } else {
+        mp.tc.bgen = bgen;
+        mp.tc.sgen = sgen;
+        mp.tc.ws = ctx.ws.p;
+        const CUtensorMap map = make_map(X, mp);
+        if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
+            fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
+        check_launch("mttkrp_tc");
+    }
+    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
+    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.I, C, dout, s);
+    check_launch("slot_reduce");
+    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
+}
+
+static void fill_times(Context& ctx, int algo, int mode, int N, dmtk_gpu_times* tm, double wall) {
+    float a, b, c, d;
+    CK(cudaEventElapsedTime(&a, ctx.ev[0], ctx.ev[1]));
+    CK(cudaEventElapsedTime(&b, ctx.ev[1], ctx.ev[2]));
+    CK(cudaEventElapsedTime(&c, ctx.ev[2], ctx.ev[3]));
+    CK(cudaEventElapsedTime(&d, ctx.ev[3], ctx.ev[4]));
+    dmtk_gpu_times t{};
+    algo = resolve_algo(algo, mode, N);
+    const bool boundary = (mode == 0 || mode == N - 1);
+    if (algo == DMTK_GPU_BASELINE) {
+        t.reorder = boundary ? 0.0 : a * 1e-3;
+        t.krp_full = b * 1e-3;
+        t.matmul = (c + d) * 1e-3;
+    } else if (algo == DMTK_GPU_ONE_STEP) {
+        // interior one-step materialises the right partial KRP (krp_partial)
+        if (!boundary) t.krp_partial = (a + b) * 1e-3;
+        t.matmul = c * 1e-3;
+        t.reduce = d * 1e-3;
+    } else {
+        t.krp_partial = (a + b) * 1e-3;
+        t.matmul = c * 1e-3;
+        t.matvec = d * 1e-3;  // the multi-TTV finish (slot reduction)
+    }
+    t.total = wall;
+    const double known = t.matmul + t.krp_full + t.krp_partial + t.matvec + t.reduce + t.reorder;
+    t.other = std::max(0.0, wall - known);
+    *tm = t;
+}
+
+static void krp_materialize(const std::vector<const double*>& U, const std::vector<long long>& rows, int C, double* out,
+                            DevBuf& scratch, cudaStream_t s) {
+    const int z = static_cast<int>(U.size());
+    if (z == 1) {
+        CK(cudaMemcpyAsync(out, U[0], static_cast<size_t>(rows[0] * C) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    // levels P(0) = U0 (.) U1, P(z) = P(z-1) (.) U_{z+1}; ping-pong in scratch
+    long long prow = rows[0];
+    const double* P = U[0];
+    long long need = 0, acc = rows[0];
+    for (int k = 1; k < z - 1; ++k) {
+        acc *= rows[k];
+        need = std::max(need, acc);
+    }
+    if (z > 2) scratch.ensure(static_cast<size_t>(2 * need * C));
+    double* bufs[2] = {scratch.p, scratch.p ? scratch.p + need * C : nullptr};
+    for (int k = 1; k < z; ++k) {
+        const long long nrow = prow * rows[k];
+        double* dst = (k == z - 1) ? out : bufs[k & 1];
+        launch_krp_level(P, U[k], dst, nrow, rows[k], C, s);
+        check_launch("krp_level");
+        P = dst;
+        prow = nrow;
+    }
+}
+
+static void validate_factors(const dmtk_gpu_tensor_s* t, int nfactors, const double* const* factors,
+                             const int64_t* frows, const int64_t* fcols, int64_t mode, int threads, const char* who) {
+    const std::string w(who);
+    if (!t) fail(DMTK_GPU_EINVAL, w + ": null tensor");
+    const int N = static_cast<int>(t->dims.size());
+    if (mode < 0 || mode >= N)
+        fail(DMTK_GPU_ERANGE, w + ": mode " + std::to_string(mode) + " outside [0, " + std::to_string(N) + ")");
+    if (nfactors != N)
+        fail(DMTK_GPU_EINVAL,
+             w + ": got " + std::to_string(nfactors) + " factors for an order-" + std::to_string(N) + " tensor");
+    const long long rank = fcols[0];
+    if (rank < 1) fail(DMTK_GPU_EINVAL, w + ": rank must be >= 1");
+    for (int k = 0; k < N; ++k) {
+        if (frows[k] != t->dims[k])
+            fail(DMTK_GPU_EINVAL, w + ": factor " + std::to_string(k) + " has " + std::to_string(frows[k]) +
+                                      " rows, mode extent is " + std::to_string(t->dims[k]));
+        if (fcols[k] != rank)
+            fail(DMTK_GPU_EINVAL, w + ": factor " + std::to_string(k) + " has rank " + std::to_string(fcols[k]) +
+                                      ", expected " + std::to_string(rank));
+        if (!factors[k]) fail(DMTK_GPU_EINVAL, w + ": factor " + std::to_string(k) + " is null");
+    }
+    if (threads < 1) fail(DMTK_GPU_EINVAL, w + ": threads must be >= 1");
+}
+
+static void inject_fault(double* m, long long n) {
+    // mttkrp.cpp:110-118
+    const char* env = std::getenv("DMTK_INJECT_FAULT");
+    if (env && *env && *env != '0' && n > 0) m[0] += 1e-3 * (1.0 + std::fabs(m[0]));
+}
+
+// Upload host factors into ctx.fac; fill device pointer table.
+static void upload_factors(Context& ctx, const dmtk_gpu_tensor_s& t, const double* const* factors, long long C,
+                           std::vector<const double*>& dptr) {
+    const int N = static_cast<int>(t.dims.size());
+    long long tot = 0;
+    for (int k = 0; k < N; ++k) tot += t.dims[k] * C;
+    ctx.fac.ensure(static_cast<size_t>(tot));
+    dptr.resize(N);
+    long long off = 0;
+    for (int k = 0; k < N; ++k) {
+        CK(cudaMemcpyAsync(ctx.fac.p + off, factors[k], static_cast<size_t>(t.dims[k] * C) * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx.stream));
+        dptr[k] = ctx.fac.p + off;
+        off += t.dims[k] * C;
+    }
+}
+
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// -------------------------------------------------------------- CP-ALS
+struct AlsOut {
+    std::vector<double> fits, iter_s, mode_s;
+    bool zero = false;
+    double norm = 0;
+};
+
+static double tensor_norm_dev(dmtk_gpu_tensor_s& t, Context& ctx) {
+    const int parts = ctx.sms * 4;
+    ctx.norm_parts.ensure(parts + 1);
+    launch_tensor_norm(t.d, t.total, ctx.norm_parts.p, parts, ctx.norm_parts.p + parts, ctx.stream);
+    count_launch(2);
+    ck(cudaGetLastError(), "tensor_norm");
+    double v = 0;
+    CK(cudaMemcpyAsync(&v, ctx.norm_parts.p + parts, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    return v;
+}
+
+// H = Hadamard of Grams of all factors except skip (linalg.cpp:228-248).
+static void gram_hadamard_dev(Context& ctx, const std::vector<long long>& rows, const std::vector<const double*>& U,
+                              int C, int skip, double* H, cudaStream_t s) {
+    bool first = true;
+    for (int k = 0; k < static_cast<int>(U.size()); ++k) {
+        if (k == skip) continue;
+        launch_gram_hadamard_accum(U[k], rows[k], C, H, first, s);
+        check_launch("gram_hadamard");
+        first = false;
+    }
+    if (first) {
+        launch_fill(H, static_cast<long long>(C) * C, 1.0, s);
+        check_launch("fill");
+    }
+}
+
+}  // namespace dmtkg
+
+using namespace dmtkg;
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* dmtk_gpu_last_error(void) { return g_last_error.c_str(); }
+int dmtk_gpu_version(void) { return 1; }
+int64_t dmtk_gpu_launch_count(void) { return g_launches.load(); }
+
+int dmtk_gpu_device_count(int* count) {
+    return guarded([&] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const double* host, dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        auto d = checked_dims(ndim, dims);
+        if (!host) fail(DMTK_GPU_EINVAL, "DenseTensor: null data");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        auto t = std::make_unique<dmtk_gpu_tensor_s>();
+        t->device = device;
+        t->dims = d;
+        t->total = prod(d, 0, ndim);
+        double* p = nullptr;
+        CK(cudaMalloc(&p, static_cast<size_t>(t->total) * sizeof(double)));
+        t->d = p;
+        t->owned = true;
+        CK(cudaMemcpyAsync(p, host, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+        *out = t.release();
+    });
+}
+
+int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double* device_ptr, dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        auto d = checked_dims(ndim, dims);
+        if (!device_ptr) fail(DMTK_GPU_EINVAL, "DenseTensor: null data");
+        context(device);
+        auto t = std::make_unique<dmtk_gpu_tensor_s>();
+        t->device = device;
+        t->dims = d;
+        t->total = prod(d, 0, ndim);
+        t->d = device_ptr;
+        t->owned = false;
+        *out = t.release();
+    });
+}
+
+int dmtk_gpu_tensor_free(dmtk_gpu_tensor t) {
+    return guarded([&] {
+        if (!t) return;
+        if (t->owned && t->d) {
+            cudaSetDevice(t->device);
+            cudaFree(const_cast<double*>(t->d));
+        }
+        delete t;
+    });
+}
+
+int dmtk_gpu_tensor_info(dmtk_gpu_tensor t, int* ndim, int64_t* dims_out8, const double** device_ptr) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "null tensor");
+        if (ndim) *ndim = static_cast<int>(t->dims.size());
+        if (dims_out8)
+            for (size_t k = 0; k < t->dims.size() && k < 8; ++k) dims_out8[k] = t->dims[k];
+        if (device_ptr) *device_ptr = t->d;
+    });
+}
+
+int dmtk_gpu_choose_order(int ndim, const int64_t* dims, int64_t mode, int* order) {
+    return guarded([&] {
+        auto d = checked_dims(ndim, dims);
+        if (mode < 0 || mode >= ndim) fail(DMTK_GPU_ERANGE, "choose_order: mode out of range");
+        *order = prod(d, 0, static_cast<int>(mode)) > prod(d, static_cast<int>(mode) + 1, ndim) ? DMTK_GPU_ORDER_LEFT
+                                                                                                : DMTK_GPU_ORDER_RIGHT;
+    });
+}
+
+int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factors, const int64_t* factor_rows,
+                    const int64_t* factor_cols, int64_t mode, int algo, int order, int threads, double* out,
+                    dmtk_gpu_times* times) {
+    return guarded([&] {
+        validate_factors(t, nfactors, factors, factor_rows, factor_cols, mode, threads, "mttkrp");
+        const int N = static_cast<int>(t->dims.size());
+        if (algo < 0 || algo > 3) fail(DMTK_GPU_EINVAL, "mttkrp: unknown algorithm");
+        const int ralgo = resolve_algo(algo, static_cast<int>(mode), N);
+        if (ralgo == DMTK_GPU_TWO_STEP && (mode == 0 || mode == N - 1))
+            fail(DMTK_GPU_EINVAL, "mttkrp_two_step: mode " + std::to_string(mode) +
+                                      " is a boundary mode with a degenerate partial KRP; use one_step instead");
+        const double t0 = now_s();
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        const long long C = factor_cols[0];
+        std::vector<const double*> dptr;
+        upload_factors(ctx, *t, factors, C, dptr);
+        const long long rows = t->dims[mode];
+        ctx.out.ensure(static_cast<size_t>(rows * C));
+        Phases ph;
+        ph.record = times != nullptr;
+        mttkrp_enqueue(*t, ctx, dptr.data(), static_cast<int>(C), static_cast<int>(mode), algo, order, ctx.out.p,
+                       ctx.stream, &ph);
+        CK(cudaMemcpyAsync(out, ctx.out.p, static_cast<size_t>(rows * C) * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+        inject_fault(out, rows * C);
+        if (times) fill_times(ctx, algo, static_cast<int>(mode), N, times, now_s() - t0);
+    });
+}
+
+int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode, int algo,
+                           int order, double* device_out, void* stream) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "mttkrp: null tensor");
+        const int N = static_cast<int>(t->dims.size());
+        if (mode < 0 || mode >= N)
+            fail(DMTK_GPU_ERANGE, "mttkrp: mode " + std::to_string(mode) + " outside [0, " + std::to_string(N) + ")");
+        if (rank < 1) fail(DMTK_GPU_EINVAL, "mttkrp: rank must be >= 1");
+        const int ralgo = resolve_algo(algo, static_cast<int>(mode), N);
+        if (ralgo == DMTK_GPU_TWO_STEP && (mode == 0 || mode == N - 1))
+            fail(DMTK_GPU_EINVAL, "mttkrp_two_step: mode " + std::to_string(mode) +
+                                      " is a boundary mode with a degenerate partial KRP; use one_step instead");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx.stream;
+        mttkrp_enqueue(*t, ctx, device_factors, static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out,
+                       s, nullptr);
+    });
+}
+
+int dmtk_gpu_krp_device(int z, const double* const* device_inputs, const int64_t* rows, int64_t cols, double* device_out,
+                        double* device_scratch, void* stream) {
+    return guarded([&] {
+        if (z < 1) fail(DMTK_GPU_EINVAL, "krp: empty input list");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (z == 1) {
+            CK(cudaMemcpyAsync(device_out, device_inputs[0], static_cast<size_t>(rows[0] * cols) * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+            return;
+        }
+        long long prow = rows[0], need = 0, acc = rows[0];
+        for (int k = 1; k < z - 1; ++k) {
+            acc *= rows[k];
+            need = std::max(need, acc);
+        }
+        if (z > 2 && !device_scratch) fail(DMTK_GPU_EINVAL, "krp: scratch required for z > 2");
+        const double* P = device_inputs[0];
+        double* bufs[2] = {device_scratch, device_scratch ? device_scratch + need * cols : nullptr};
+        for (int k = 1; k < z; ++k) {
+            const long long nrow = prow * rows[k];
+            double* dst = (k == z - 1) ? device_out : bufs[k & 1];
+            launch_krp_level(P, device_inputs[k], dst, nrow, rows[k], static_cast<int>(cols), s);
+            check_launch("krp_level");
+            P = dst;
+            prow = nrow;
+        }
+    });
+}
+
+int dmtk_gpu_krp(int device, int z, const double* const* inputs, const int64_t* rows, int64_t cols, int variant,
+                 double* out, uint64_t* hadamards) {
+    return guarded([&] {
+        // validation order and messages of radices_of (krp.cpp:16-36)
+        if (z < 1) fail(DMTK_GPU_EINVAL, "krp: empty input list");
+        for (int k = 0; k < z; ++k) {
+            if (!inputs[k]) fail(DMTK_GPU_EINVAL, "krp: null input");
+            if (rows[k] < 1) fail(DMTK_GPU_EINVAL, "krp: input " + std::to_string(k) + " has no rows");
+        }
+        long long total = 1;
+        for (int k = 0; k < z; ++k) {
+            if (__builtin_mul_overflow(total, rows[k], &total)) fail(DMTK_GPU_EOVERFLOW, "krp: row count overflows");
+        }
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        long long in_tot = 0;
+        for (int k = 0; k < z; ++k) in_tot += rows[k] * cols;
+        ctx.fac.ensure(static_cast<size_t>(in_tot));
+        std::vector<const double*> dptr(z);
+        long long off = 0;
+        for (int k = 0; k < z; ++k) {
+            CK(cudaMemcpyAsync(ctx.fac.p + off, inputs[k], static_cast<size_t>(rows[k] * cols) * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx.stream));
+            dptr[k] = ctx.fac.p + off;
+            off += rows[k] * cols;
+        }
+        ctx.out.ensure(static_cast<size_t>(std::max<long long>(total * cols, 1)));
+        std::vector<long long> r(rows, rows + z);
+        if (cols > 0) krp_materialize(dptr, r, static_cast<int>(cols), ctx.out.p, ctx.scratch, ctx.stream);
+        if (total * cols > 0)
+            CK(cudaMemcpyAsync(out, ctx.out.p, static_cast<size_t>(total * cols) * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+        if (hadamards) {
+            // KrpStats semantics (krp.hpp:15-17): reuse = one product per row
+            // of every level P(0..Z-3) plus one per output row (= the
+            // single-thread count of krp.cpp:99-143); naive = (Z-1) per row.
+            uint64_t h = 0;
+            if (variant == 1 && z >= 3) {
+                h = static_cast<uint64_t>(total) * static_cast<uint64_t>(z - 1);
+            } else if (z >= 2) {
+                long long acc = rows[0];
+                for (int k = 1; k < z; ++k) {
+                    acc *= rows[k];
+                    h += static_cast<uint64_t>(acc);
+                }
+            }
+            *hadamards = h;
+        }
+    });
+}
+
+int dmtk_gpu_tensor_norm(dmtk_gpu_tensor t, double* out) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "tensor_norm: null tensor");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        *out = tensor_norm_dev(*t, ctx);
+    });
+}
+
+int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t rank, const double* const* factors,
+                           int64_t skip, double* h_out) {
+    return guarded([&] {
+        if (ndim < 1) fail(DMTK_GPU_EINVAL, "gram_hadamard: no factors");
+        if (rank < 1 || rank > 64) fail(DMTK_GPU_EINVAL, "gram_hadamard: rank must be in [1, 64] on the GPU path");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        long long tot = 0;
+        for (int k = 0; k < ndim; ++k) tot += rows[k] * rank;
+        ctx.fac.ensure(static_cast<size_t>(tot));
+        std::vector<const double*> dp(ndim);
+        std::vector<long long> r(rows, rows + ndim);
+        long long off = 0;
+        for (int k = 0; k < ndim; ++k) {
+            CK(cudaMemcpyAsync(ctx.fac.p + off, factors[k], static_cast<size_t>(rows[k] * rank) * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx.stream));
+            dp[k] = ctx.fac.p + off;
+            off += rows[k] * rank;
+        }
+        ctx.als_small.ensure(64 * 64);
+        gram_hadamard_dev(ctx, r, dp, static_cast<int>(rank), static_cast<int>(skip), ctx.als_small.p, ctx.stream);
+        CK(cudaMemcpyAsync(h_out, ctx.als_small.p, static_cast<size_t>(rank * rank) * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+    });
+}
+
+int dmtk_gpu_solve_psd(int device, int64_t rank, const double* h, int64_t rows, const double* m, double* u_out) {
+    return guarded([&] {
+        if (rank < 1 || rank > 64) fail(DMTK_GPU_EINVAL, "solve_psd: rank must be in [1, 64] on the GPU path");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        ctx.als_small.ensure(64 * 64 * 4);
+        ctx.scratch.ensure(static_cast<size_t>(2 * rows * rank + 3 * 64 * 64));
+        double* H = ctx.als_small.p;
+        double* M = ctx.scratch.p;
+        double* U = M + rows * rank;
+        double* S = U + rows * rank;
+        CK(cudaMemcpyAsync(H, h, static_cast<size_t>(rank * rank) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        CK(cudaMemcpyAsync(M, m, static_cast<size_t>(rows * rank) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        launch_solve_psd(H, static_cast<int>(rank), M, rows, U, S, ctx.flag, ctx.stream);
+        count_launch(4);
+        ck(cudaGetLastError(), "solve_psd");
+        CK(cudaMemcpyAsync(u_out, U, static_cast<size_t>(rows * rank) * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+    });
+}
+
+int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out,
+                    double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
+                    int* zero_tensor, double* tensor_norm_out) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "cp_als: null tensor");
+        if (cfg->rank < 1) fail(DMTK_GPU_EINVAL, "cp_als: rank must be >= 1");
+        if (cfg->max_iters < 0) fail(DMTK_GPU_EINVAL, "cp_als: max_iters must be >= 0");
+        if (cfg->threads < 1) fail(DMTK_GPU_EINVAL, "cp_als: threads must be >= 1");
+        if (cfg->rank > 64) fail(DMTK_GPU_EINVAL, "cp_als: rank above 64 is not supported on the GPU path");
+        const int N = static_cast<int>(t->dims.size());
+        if (cfg->algo == DMTK_GPU_TWO_STEP)  // the first (boundary) mode refuses two_step
+            fail(DMTK_GPU_EINVAL,
+                 "mttkrp_two_step: mode 0 is a boundary mode with a degenerate partial KRP; use one_step instead");
+        const int C = static_cast<int>(cfg->rank);
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        cudaStream_t s = ctx.stream;
+
+        // KruskalModel::random (cp_als.cpp:87-99): one mt19937_64 stream
+        std::mt19937_64 rng(cfg->seed);
+        long long ftot = 0, maxrows = 0;
+        for (int k = 0; k < N; ++k) {
+            ftot += t->dims[k] * C;
+            maxrows = std::max(maxrows, t->dims[k]);
+        }
+        std::vector<double> hf(static_cast<size_t>(ftot));
+        for (auto& v : hf) v = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+
+        const double normx = tensor_norm_dev(*t, ctx);
+        *tensor_norm_out = normx;
+        *n_iters = 0;
+        *zero_tensor = 0;
+        if (normx == 0.0) {  // cp_als.cpp:183-189
+            std::fill(factors_out, factors_out + ftot, 0.0);
+            std::fill(lambda_out, lambda_out + C, 0.0);
+            *zero_tensor = 1;
+            return;
+        }
+        // device state: factors | lambda | M | H | normx | fit(iters x 4) | solve scratch
+        DevBuf F, M, aux;
+        F.ensure(static_cast<size_t>(ftot));
+        M.ensure(static_cast<size_t>(maxrows * C));
+        const int iters = cfg->max_iters;
+        aux.ensure(static_cast<size_t>(64 + 64 * 64 + 1 + 4 * std::max(iters, 1) + 3 * 64 * 64 + 64));
+        double* lam = aux.p;
+        double* H = lam + 64;
+        double* dnorm = H + 64 * 64;
+        double* fitb = dnorm + 1;
+        double* solve_scr = fitb + 4 * std::max(iters, 1);
+        CK(cudaMemcpyAsync(F.p, hf.data(), hf.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dnorm, &normx, sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_fill(lam, C, 1.0, s);
+        check_launch("fill");
+        std::vector<const double*> Uc(N);
+        std::vector<double*> Um(N);
+        long long off = 0;
+        for (int k = 0; k < N; ++k) {
+            Um[k] = F.p + off;
+            Uc[k] = Um[k];
+            off += t->dims[k] * C;
+        }
+        std::vector<cudaEvent_t> evs(static_cast<size_t>(N + 1));
+        for (auto& e : evs) CK(cudaEventCreate(&e));
+        double prev_fit = 0.0;
+        int done = 0;
+        for (int iter = 1; iter <= iters; ++iter) {
+            for (int n = 0; n < N; ++n) {  // als_iterate, cp_als.cpp:134-153
+                CK(cudaEventRecord(evs[n], s));
+                mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
+                gram_hadamard_dev(ctx, t->dims, Uc, C, n, H, s);
+                launch_solve_psd(H, C, M.p, t->dims[n], Um[n], solve_scr, ctx.flag, s);
+                count_launch(4);
+                ck(cudaGetLastError(), "solve_psd");
+                launch_normalize(Um[n], t->dims[n], C, lam, s);
+                check_launch("normalize");
+            }
+            CK(cudaEventRecord(evs[N], s));
+            // H, M hold the last mode's values (cp_als.cpp:149-155)
+            launch_fit(Um[N - 1], M.p, t->dims[N - 1], C, lam, H, dnorm, fitb + 4 * (iter - 1), s);
+            check_launch("fit");
+            double f4[4];
+            CK(cudaMemcpyAsync(f4, fitb + 4 * (iter - 1), sizeof(f4), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            float ms_total = 0;
+            for (int n = 0; n < N; ++n) {
+                float ms;
+                CK(cudaEventElapsedTime(&ms, evs[n], evs[n + 1]));
+                if (mode_seconds_out) mode_seconds_out[(iter - 1) * N + n] = ms * 1e-3;
+                ms_total += ms;
+            }
+            if (iter_seconds_out) iter_seconds_out[iter - 1] = ms_total * 1e-3;
+            fits_out[iter - 1] = f4[0];
+            done = iter;
+            if (iter > 1 && std::fabs(f4[0] - prev_fit) < cfg->tol) break;
+            prev_fit = f4[0];
+        }
+        for (auto& e : evs) cudaEventDestroy(e);
+        CK(cudaMemcpyAsync(factors_out, F.p, static_cast<size_t>(ftot) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (done > 0) {
+            CK(cudaMemcpyAsync(lambda_out, lam, static_cast<size_t>(C) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        } else {
+            std::fill(lambda_out, lambda_out + C, 1.0);
+        }
+        CK(cudaStreamSynchronize(s));
+        *n_iters = done;
+    });
+}
+
+int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, const int64_t* factor_rows,
+                 const int64_t* factor_cols, const double* lambda, int64_t nlambda, int threads, double* out4) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "fit: null tensor");
+        const int N = static_cast<int>(t->dims.size());
+        if (nfactors != N)  // validate_model, cp_als.cpp:74-83
+            fail(DMTK_GPU_EINVAL, "model has " + std::to_string(nfactors) + " factors for an order-" +
+                                      std::to_string(N) + " tensor");
+        const long long C = nfactors > 0 ? factor_cols[0] : 0;
+        if (nlambda != C) fail(DMTK_GPU_EINVAL, "model lambda length does not match rank");
+        validate_factors(t, nfactors, factors, factor_rows, factor_cols, N - 1, threads, "mttkrp");
+        if (C > 64) fail(DMTK_GPU_EINVAL, "fit: rank above 64 is not supported on the GPU path");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        const double normx = tensor_norm_dev(*t, ctx);
+        std::vector<const double*> dptr;
+        upload_factors(ctx, *t, factors, C, dptr);
+        const long long rows = t->dims[N - 1];
+        ctx.out.ensure(static_cast<size_t>(rows * C));
+        ctx.als_small.ensure(64 * 64 + 64 + 8);
+        double* H = ctx.als_small.p;
+        double* lam = H + 64 * 64;
+        double* dn = lam + 64;
+        double* o4 = dn + 1;
+        CK(cudaMemcpyAsync(lam, lambda, static_cast<size_t>(C) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        CK(cudaMemcpyAsync(dn, &normx, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        // cp_als.cpp:160-172: last-mode one_step MTTKRP, then the fit formula
+        mttkrp_enqueue(*t, ctx, dptr.data(), static_cast<int>(C), N - 1, DMTK_GPU_ONE_STEP, 0, ctx.out.p, ctx.stream,
+                       nullptr);
+        gram_hadamard_dev(ctx, t->dims, dptr, static_cast<int>(C), N - 1, H, ctx.stream);
+        launch_fit(dptr[N - 1], ctx.out.p, rows, static_cast<int>(C), lam, H, dn, o4, ctx.stream);
+        check_launch("fit");
+        CK(cudaMemcpyAsync(out4, o4, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+    });
+}
+
+int dmtk_gpu_fp64_peak(int device, double* tflops) {
+    return guarded([&] {
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        ctx.als_small.ensure(64);
+        const int blocks = ctx.sms * 2, iters = 20000;
+        launch_dmma_peak(ctx.als_small.p, blocks, 200, ctx.stream);
+        count_launch();
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, ctx.stream));
+        launch_dmma_peak(ctx.als_small.p, blocks, iters, ctx.stream);
+        count_launch();
+        CK(cudaEventRecord(b, ctx.stream));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        const double flops = 2.0 * 256 * 8 * static_cast<double>(iters) * blocks * (256 / 32);
+        *tflops = flops / (ms * 1e-3) / 1e12;
+    });
+}
+
+}  // extern "C"

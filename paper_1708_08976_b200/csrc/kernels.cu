@@ -1,0 +1,469 @@
+// kernels.cu -- the non-streaming kernels of the dmtk B200 path:
+//   * Khatri-Rao product levels (reference krp.cpp:99-181, bitwise contract)
+//   * generic MTTKRP for shapes the TMA path cannot address
+//   * the deterministic CSR slot reduction that finishes every MTTKRP
+//   * the baseline algorithm's explicit matricization (mttkrp.cpp:262-291)
+//   * CP-ALS pieces: Gram / Gram-Hadamard, Cholesky + Jacobi solve,
+//     column normalisation, reconstruction-free fit, tensor norm
+//     (linalg.cpp:210-387, cp_als.cpp:21-118)
+//   * an FP64 tensor-core peak probe used for the roofline denominator.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dmtkg {
+
+// ---------------------------------------------------------------- KRP
+// One reuse level: out(row, c) = P(row / J, c) * U(row % J, c). Applied
+// level by level this is the cached-partial generator of krp.cpp:53-88 (each
+// level's rows are the partial products P(z) of krp.hpp:27-31) with the same
+// left-to-right association, hence bitwise equal to oracle::krp_kron.
+__global__ void krp_level_kernel(const double* __restrict__ P, const double* __restrict__ U, double* __restrict__ out,
+                                 long long rows_out, long long J, int C) {
+    const long long total = rows_out * C;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    if ((C & 1) == 0) {
+        const long long half = total >> 1;
+        for (long long e2 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e2 < half; e2 += stride) {
+            const long long e = e2 << 1;
+            const long long row = e / C;
+            const int c = static_cast<int>(e - row * C);
+            const long long q = row / J;
+            const long long r = row - q * J;
+            const double2 a = *reinterpret_cast<const double2*>(P + q * C + c);
+            const double2 b = *reinterpret_cast<const double2*>(U + r * C + c);
+            double2 o;
+            o.x = a.x * b.x;
+            o.y = a.y * b.y;
+            __stcs(reinterpret_cast<double2*>(out + e), o);
+        }
+        return;
+    }
+    for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const long long row = e / C;
+        const int c = static_cast<int>(e - row * C);
+        const long long q = row / J;
+        out[e] = P[q * C + c] * U[(row - q * J) * C + c];
+    }
+}
+
+// ----------------------------------------------------------- generic MTTKRP
+// M(i,c) partial over a chunk of j: sum_j KR(j,c) * sum_l X(l,i,j) KL(l,c).
+// Slot layout ws[(jc * I + i) * C + c]; the CSR reduce finishes the sum.
+__global__ void mttkrp_generic_kernel(const double* __restrict__ X, long long L, long long I, long long R, int C,
+                                      KrpGen kl, KrpGen kr, long long jchunk, double* __restrict__ ws) {
+    const long long jc = blockIdx.x;
+    const long long e = static_cast<long long>(blockIdx.y) * blockDim.x + threadIdx.x;
+    if (e >= I * C) return;
+    const long long i = e / C;
+    const int c = static_cast<int>(e - i * C);
+    const long long j0 = jc * jchunk;
+    const long long j1 = j0 + jchunk < R ? j0 + jchunk : R;
+    double acc = 0.0;
+    for (long long j = j0; j < j1; ++j) {
+        const double* xs = X + (j * I + i) * L;
+        double s = 0.0;
+        for (long long l = 0; l < L; ++l) s += xs[l] * krp_value(kl, l, c);
+        acc += s * krp_value(kr, j, c);
+    }
+    ws[(jc * I + i) * C + c] = acc;
+}
+
+// ------------------------------------------------------------ CSR reduce
+// out(i, c) = sum_{e in [rowptr[i], rowptr[i+1])} ws(slot[e], c), fixed order.
+__global__ void slot_reduce_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
+                                   const long long* __restrict__ slots, long long rows, int C, double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= rows * C) return;
+    const long long i = e / C;
+    const int c = static_cast<int>(e - i * C);
+    double s = 0.0;
+    for (long long k = rowptr[i]; k < rowptr[i + 1]; ++k) s += ws[slots[k] * C + c];
+    out[e] = s;
+}
+
+// ----------------------------------------------------------- baseline reorder
+// dst = col-major X_(n): column q = l + L*j, dst[q*I + i] = X(l, i, j)
+// (mttkrp.cpp:272-290), done as a tiled transpose of every j-slab.
+__global__ void matricize_kernel(const double* __restrict__ X, long long L, long long I, long long R,
+                                 double* __restrict__ dst) {
+    __shared__ double tile[32][33];
+    const long long j = blockIdx.z;
+    const long long l0 = static_cast<long long>(blockIdx.x) * 32;
+    const long long i0 = static_cast<long long>(blockIdx.y) * 32;
+    const double* src = X + j * L * I;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const long long i = i0 + y, l = l0 + threadIdx.x;
+        if (i < I && l < L) tile[y][threadIdx.x] = src[i * L + l];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const long long l = l0 + y, i = i0 + threadIdx.x;
+        if (i < I && l < L) dst[(l + L * j) * I + i] = tile[threadIdx.x][y];
+    }
+}
+
+// --------------------------------------------------------------- CP-ALS
+// G = U^T U (linalg.cpp:210-226): upper triangle accumulated over rows in
+// order, mirrored so the result is symmetric to the last bit. Then H *= G.
+__global__ void gram_hadamard_accum_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ H,
+                                           int first) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= C * C) return;
+    const int c1 = e / C, c2 = e % C;
+    if (c2 < c1) return;
+    double s = 0.0;
+    for (long long r = 0; r < rows; ++r) s = fma(U[r * C + c1], U[r * C + c2], s);
+    const double h = first ? s : H[c1 * C + c2] * s;
+    H[c1 * C + c2] = h;
+    if (c2 != c1) H[c2 * C + c1] = h;
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+    for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<long long>(gridDim.x) * blockDim.x)
+        p[e] = v;
+}
+
+// Cholesky with pivot floor 1e-12 * trace (linalg.cpp:254-276), one CTA.
+// Writes L (row-major, lower) and flag[0] = 1 on success, 0 on failure.
+__global__ void cholesky_kernel(const double* __restrict__ H, int n, double* __restrict__ Lm, int* __restrict__ flag) {
+    __shared__ double sL[64 * 64];
+    __shared__ double s_root;
+    __shared__ int s_ok;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) sL[e] = 0.0;
+    if (tid == 0) s_ok = 1;
+    double tr = 0.0;
+    for (int k = 0; k < n; ++k) tr += H[k * n + k];
+    const double tol = 1e-12 * tr;
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        if (tid == 0) {
+            double d = H[j * n + j];
+            for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
+            if (d <= tol) {
+                s_ok = 0;
+            } else {
+                s_root = sqrt(d);
+                sL[j * n + j] = s_root;
+            }
+        }
+        __syncthreads();
+        if (!s_ok) break;
+        for (int i = j + 1 + tid; i < n; i += blockDim.x) {
+            double s = H[i * n + j];
+            for (int k = 0; k < j; ++k) s -= sL[i * n + k] * sL[j * n + k];
+            sL[i * n + j] = s / s_root;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < n * n; e += blockDim.x) Lm[e] = sL[e];
+    if (tid == 0) flag[0] = s_ok;
+}
+
+// Row-wise forward then back substitution (linalg.cpp:340-354).
+__global__ void chol_solve_rows_kernel(const double* __restrict__ Lm, int n, const double* __restrict__ M, long long rows,
+                                       double* __restrict__ U, const int* __restrict__ flag) {
+    if (!flag[0]) return;
+    const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    double w[64];
+    const double* mrow = M + r * n;
+    double* urow = U + r * n;
+    for (int j = 0; j < n; ++j) {
+        double s = mrow[j];
+        for (int k = 0; k < j; ++k) s -= Lm[j * n + k] * w[k];
+        w[j] = s / Lm[j * n + j];
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        double s = w[j];
+        for (int k = j + 1; k < n; ++k) s -= Lm[k * n + j] * urow[k];
+        urow[j] = s / Lm[j * n + j];
+    }
+}
+
+// Cyclic Jacobi pseudoinverse fallback (linalg.cpp:281-326, 358-386), one
+// CTA; only runs when the Cholesky flag is 0. Produces V and gain.
+__global__ void jacobi_kernel(const double* __restrict__ H, int n, double* __restrict__ Vout, double* __restrict__ gain,
+                              const int* __restrict__ flag) {
+    if (flag[0]) return;
+    __shared__ double a[64 * 64];
+    double* v = Vout;  // eigenvectors rotated in place in global memory
+    __shared__ double s_cs, s_sn;
+    __shared__ int s_done;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        a[e] = H[e];
+        v[e] = (e / n == e % n) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int sweep = 0; sweep < 128; ++sweep) {
+        if (tid == 0) {
+            double off = 0.0, diag = 0.0;
+            for (int p = 0; p < n; ++p)
+                for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
+            for (int p = 0; p < n; ++p) diag += a[p * n + p] * a[p * n + p];
+            s_done = (off <= 1e-300) || (off <= 1e-30 * (diag > 1e-300 ? diag : 1e-300));
+        }
+        __syncthreads();
+        if (s_done) break;
+        for (int p = 0; p < n; ++p) {
+            for (int q = p + 1; q < n; ++q) {
+                if (tid == 0) {
+                    const double apq = a[p * n + q];
+                    if (apq == 0.0) {
+                        s_cs = 1.0;
+                        s_sn = 0.0;
+                    } else {
+                        const double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+                        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        s_cs = 1.0 / sqrt(t * t + 1.0);
+                        s_sn = t * s_cs;
+                    }
+                }
+                __syncthreads();
+                const double cs = s_cs, sn = s_sn;
+                if (sn != 0.0 || cs != 1.0) {
+                    for (int r = tid; r < n; r += blockDim.x) {
+                        const double arp = a[r * n + p], arq = a[r * n + q];
+                        a[r * n + p] = cs * arp - sn * arq;
+                        a[r * n + q] = sn * arp + cs * arq;
+                    }
+                    __syncthreads();
+                    for (int c = tid; c < n; c += blockDim.x) {
+                        const double apc = a[p * n + c], aqc = a[q * n + c];
+                        a[p * n + c] = cs * apc - sn * aqc;
+                        a[q * n + c] = sn * apc + cs * aqc;
+                    }
+                    for (int r = tid; r < n; r += blockDim.x) {
+                        const double vrp = v[r * n + p], vrq = v[r * n + q];
+                        v[r * n + p] = cs * vrp - sn * vrq;
+                        v[r * n + q] = sn * vrp + cs * vrq;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (tid == 0) {
+        double lam_max = 0.0;
+        for (int i = 0; i < n; ++i) lam_max = a[i * n + i] > lam_max ? a[i * n + i] : lam_max;
+        const double fl = 1e-12 * lam_max;
+        for (int i = 0; i < n; ++i) {
+            const double lam = a[i * n + i];
+            gain[i] = (lam > fl && lam > 0.0) ? 1.0 / lam : 0.0;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void jacobi_apply_rows_kernel(const double* __restrict__ V, const double* __restrict__ gain, int n,
+                                         const double* __restrict__ M, long long rows, double* __restrict__ U,
+                                         const int* __restrict__ flag) {
+    if (flag[0]) return;
+    const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    double tmp[64];
+    const double* mrow = M + r * n;
+    for (int j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int c = 0; c < n; ++c) s += mrow[c] * V[c * n + j];
+        tmp[j] = s * gain[j];
+    }
+    for (int c = 0; c < n; ++c) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += tmp[j] * V[c * n + j];
+        U[r * n + c] = s;
+    }
+}
+
+// Column norms into lambda, scale columns (cp_als.cpp:101-118). One CTA.
+__global__ void normalize_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda) {
+    __shared__ double s_norm[64];
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        double sq = 0.0;
+        for (long long i = 0; i < rows; ++i) {
+            const double v = U[i * C + c];
+            sq += v * v;
+        }
+        s_norm[c] = sqrt(sq);
+        lambda[c] = s_norm[c];
+    }
+    __syncthreads();
+    for (long long e = threadIdx.x; e < rows * C; e += blockDim.x) {
+        const int c = static_cast<int>(e % C);
+        const double nrm = s_norm[c];
+        if (nrm > 0.0) U[e] *= 1.0 / nrm;
+    }
+}
+
+// Fit from the last mode (cp_als.cpp:34-72). One CTA; writes out[0..3] =
+// fit, rel_residual, abs_residual, defined. normx2 is ||X||^2 (device).
+__global__ void fit_kernel(const double* __restrict__ U, const double* __restrict__ Mlast, long long rows, int C,
+                           const double* __restrict__ lambda, const double* __restrict__ Hlast,
+                           const double* __restrict__ normx, double* __restrict__ out) {
+    __shared__ double red[256];
+    __shared__ double G[64 * 64];
+    double inner = 0.0;
+    for (long long e = threadIdx.x; e < rows * C; e += blockDim.x) {
+        const int c = static_cast<int>(e % C);
+        inner += Mlast[e] * lambda[c] * U[e];
+    }
+    red[threadIdx.x] = inner;
+    for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+        const int c1 = e / C, c2 = e % C;
+        if (c2 < c1) continue;
+        double s = 0.0;
+        for (long long r = 0; r < rows; ++r) s = fma(U[r * C + c1], U[r * C + c2], s);
+        G[c1 * C + c2] = s;
+        G[c2 * C + c1] = s;
+    }
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double in = red[0];
+        double ny = 0.0;
+        for (int c1 = 0; c1 < C; ++c1)
+            for (int c2 = 0; c2 < C; ++c2) ny += lambda[c1] * lambda[c2] * Hlast[c1 * C + c2] * G[c1 * C + c2];
+        const double nx = normx[0];
+        double res2 = nx * nx - 2.0 * in + ny;
+        if (res2 < 0.0) res2 = 0.0;
+        const double ar = sqrt(res2);
+        out[2] = ar;
+        if (nx > 0.0) {
+            out[1] = ar / nx;
+            out[0] = 1.0 - out[1];
+            out[3] = 1.0;
+        } else {
+            out[0] = 0.0;
+            out[1] = 0.0;
+            out[3] = 0.0;
+        }
+    }
+}
+
+// Sum of squares, two passes, fixed reduction order (cp_als.cpp:21-30).
+__global__ void sumsq_partial_kernel(const double* __restrict__ x, long long n, double* __restrict__ part) {
+    __shared__ double red[512];
+    double s0 = 0.0, s1 = 0.0;
+    const long long n2 = n >> 1;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n2; e += stride) {
+            const double2 v = __ldcs(x2 + e);
+            s0 = fma(v.x, v.x, s0);
+            s1 = fma(v.y, v.y, s1);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s0 = fma(x[n - 1], x[n - 1], s0);
+    } else {
+        for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+            s0 = fma(x[e], x[e], s0);
+    }
+    red[threadIdx.x] = s0 + s1;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void sumsq_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out_norm) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < n; ++k) s += part[k];
+        out_norm[0] = sqrt(s);
+    }
+}
+
+// --------------------------------------------------------- FP64 peak probe
+__global__ void dmma_peak_kernel(double* out, int iters) {
+    double acc[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = 0.0;
+    const double a = 1.0 + threadIdx.x * 1e-9, b = 0.5;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dmma_8x8x4(acc[k][0], acc[k][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += acc[k][0] + acc[k][1];
+    if (s == 1234.5678) out[0] = s;
+}
+
+// --------------------------------------------------------------- launchers
+static inline int blocks_for(long long n, int tpb, int cap = 148 * 32) {
+    long long b = (n + tpb - 1) / tpb;
+    if (b < 1) b = 1;
+    return static_cast<int>(b < cap ? b : cap);
+}
+
+void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
+                      cudaStream_t s) {
+    const long long n = rows_out * C;
+    krp_level_kernel<<<blocks_for((n + 1) / 2, 256), 256, 0, s>>>(P, U, out, rows_out, J, C);
+}
+
+void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,
+                           const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(n_jc), static_cast<unsigned>((I * C + 127) / 128));
+    mttkrp_generic_kernel<<<grid, 128, 0, s>>>(X, L, I, R, C, kl, kr, jchunk, ws);
+}
+
+void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
+                        double* out, cudaStream_t s) {
+    const long long n = rows * C;
+    slot_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, rowptr, slots, rows, C, out);
+}
+
+void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>((I + 31) / 32), static_cast<unsigned>(R));
+    matricize_kernel<<<grid, dim3(32, 8), 0, s>>>(X, L, I, R, dst);
+}
+
+void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s) {
+    gram_hadamard_accum_kernel<<<(C * C + 127) / 128, 128, 0, s>>>(U, rows, C, H, first ? 1 : 0);
+}
+
+void launch_fill(double* p, long long n, double v, cudaStream_t s) {
+    fill_kernel<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
+}
+
+void launch_solve_psd(const double* H, int n, const double* M, long long rows, double* U, double* scratch, int* flag,
+                      cudaStream_t s) {
+    double* Lm = scratch;            // n*n
+    double* V = scratch + 64 * 64;   // n*n
+    double* gain = V + 64 * 64;      // n
+    cholesky_kernel<<<1, 128, 0, s>>>(H, n, Lm, flag);
+    const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
+    chol_solve_rows_kernel<<<gb, 128, 0, s>>>(Lm, n, M, rows, U, flag);
+    jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
+    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, n, M, rows, U, flag);
+}
+
+void launch_normalize(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
+    normalize_kernel<<<1, 256, 0, s>>>(U, rows, C, lambda);
+}
+
+void launch_fit(const double* U, const double* Mlast, long long rows, int C, const double* lambda, const double* Hlast,
+                const double* normx, double* out, cudaStream_t s) {
+    fit_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, normx, out);
+}
+
+void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s) {
+    sumsq_partial_kernel<<<nparts, 512, 0, s>>>(x, n, part);
+    sumsq_final_kernel<<<1, 32, 0, s>>>(part, nparts, out);
+}
+
+void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s) {
+    dmma_peak_kernel<<<blocks, 256, 0, s>>>(out, iters);
+}
+
+}  // namespace dmtkg

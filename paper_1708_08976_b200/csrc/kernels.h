@@ -1,0 +1,33 @@
+// kernels.h -- host-side launchers for the dmtk B200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mttkrp_plan.h"
+
+namespace dmtkg {
+
+void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
+                      cudaStream_t s);
+void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,
+                           const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s);
+void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
+                        double* out, cudaStream_t s);
+void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s);
+void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s);
+void launch_fill(double* p, long long n, double v, cudaStream_t s);
+// scratch: >= 2*64*64 + 64 doubles; flag: 1 int
+void launch_solve_psd(const double* H, int n, const double* M, long long rows, double* U, double* scratch, int* flag,
+                      cudaStream_t s);
+void launch_normalize(double* U, long long rows, int C, double* lambda, cudaStream_t s);
+void launch_fit(const double* U, const double* Mlast, long long rows, int C, const double* lambda, const double* Hlast,
+                const double* normx, double* out, cudaStream_t s);
+void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s);
+void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
+
+// Tensor-core streaming MTTKRP (mttkrp_tc.cuh). nb in [1, 8], tail in
+// {0, 1, 2, 4}; returns false when no instantiation matches.
+int tc_smem_bytes(int nb, int tail);
+bool launch_mttkrp_tc(const TcPlan& p, const CUtensorMap& map, int nb, int tail, bool kmajor, int grid, cudaStream_t s);
+
+}  // namespace dmtkg
