@@ -82,9 +82,10 @@ int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factor
                     dmtk_gpu_times* times);
 
 /* Same contraction with every operand already on the device; enqueued on
- * `stream` (a cudaStream_t, NULL = the library's stream) without host
- * synchronisation. No fault hook. Used by the device-resident benchmark leg
- * and the CP-ALS driver. */
+ * `stream` (a cudaStream_t; NULL = the legacy default stream) without host
+ * synchronisation. No fault hook. The library's workspace is per device:
+ * callers order concurrent device calls on one device (one stream). Used by
+ * the device-resident benchmark leg. */
 int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode,
                            int algo, int order, double* device_out, void* stream);
 

@@ -23,12 +23,26 @@ struct KrpGen {
     long long stride[kMaxFactors];
 };
 
+// a / b for non-negative operands, 32-bit when both fit.
+__device__ __forceinline__ long long div_nn(long long a, long long b) {
+    if (a < 0x7fffffffLL && b < 0x7fffffffLL) return static_cast<unsigned>(a) / static_cast<unsigned>(b);
+    return a / b;
+}
+
+// Digit of factor f for a compound index (32-bit division when it fits).
+__device__ __forceinline__ long long krp_digit(const KrpGen& g, int f, long long idx) {
+    if (idx < 0x7fffffffLL && g.stride[f] < 0x7fffffffLL && g.ext[f] < 0x7fffffffLL) {
+        const unsigned q = static_cast<unsigned>(idx) / static_cast<unsigned>(g.stride[f]);
+        return q % static_cast<unsigned>(g.ext[f]);
+    }
+    return (idx / g.stride[f]) % g.ext[f];
+}
+
 __device__ __forceinline__ double krp_value(const KrpGen& g, long long idx, int c) {
     double v = 1.0;
 #pragma unroll 1
     for (int f = 0; f < g.nf; ++f) {
-        const long long d = (idx / g.stride[f]) % g.ext[f];
-        v *= __ldg(g.U[f] + d * g.ldu + c);
+        v *= __ldg(g.U[f] + krp_digit(g, f, idx) * g.ldu + c);
     }
     return v;
 }
@@ -38,8 +52,7 @@ __device__ __forceinline__ double krp_head(const KrpGen& g, long long idx, int c
     double v = 1.0;
 #pragma unroll 1
     for (int f = 1; f < g.nf; ++f) {
-        const long long d = (idx / g.stride[f]) % g.ext[f];
-        v *= __ldg(g.U[f] + d * g.ldu + c);
+        v *= __ldg(g.U[f] + krp_digit(g, f, idx) * g.ldu + c);
     }
     return v;
 }
@@ -84,20 +97,29 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+// L2 policy for data read exactly once (the streamed tensor): evict first,
+// so the factor rows the builders re-read stay L2-resident.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
         : "memory");
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                            int c2) {
+                                            int c2, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
         : "memory");
 }
 

@@ -877,7 +877,7 @@ int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factor
                                       " is a boundary mode with a degenerate partial KRP; use one_step instead");
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx.stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
         mttkrp_enqueue(*t, ctx, device_factors, static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out,
                        s, nullptr);
     });

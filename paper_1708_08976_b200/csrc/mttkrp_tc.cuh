@@ -6,12 +6,12 @@
 //   warps 0-3  consumers: 32 tile rows each x all C columns. Columns in
 //              groups of 8 run on DMMA; the C % 8 remainder ("tail") runs on
 //              DFMA so no tensor-core work is wasted on padding.
-//   warps 4-5  builders: write the stage's B tile (32 KRP rows x C) into
-//              shared memory in DMMA fragment order, one multiply per entry
-//              (cached head partial x fastest factor row: the paper's
-//              reuse scheme, Alg. 1, reference krp.cpp:53-88).
+//   warps 4-5  builders, alternating stages: write the stage's B tile (32
+//              KRP rows x C) into shared memory in DMMA fragment order, one
+//              multiply per entry (cached head partial x fastest factor row:
+//              the paper's reuse scheme, Alg. 1, krp.cpp:53-88).
 //   warp 6     producer: one elected lane issues the TMA box loads.
-// Per stage: full barrier (TMA bytes + 2 builder arrivals), empty barrier
+// Per stage: full barrier (TMA bytes + 1 builder arrival), empty barrier
 // (4 consumer arrivals).
 //
 // The A tile arrives through 128-byte-swizzled TMA boxes; the k index a
@@ -38,15 +38,49 @@ struct TcCfg {
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + HEAD_BYTES + BAR_BYTES + 1024;
 };
 
+// Which contraction row of a 32-row stage DMMA lane column t reads at k4-step
+// s. Chosen so that each half-warp's 16 fragment loads hit 32 distinct
+// banks under the 128-byte TMA swizzle (2 wavefronts per LDS.64, the
+// minimum): M-major tiles are [k][16 m] boxes, K-major tiles [row][16 k].
+template <bool KMAJ>
+__device__ __forceinline__ int kperm(int s, int t) {
+    return KMAJ ? 16 * (s >> 2) + 8 * (t >> 1) + (t & 1) + 2 * (s & 3) : 8 * (s >> 1) + 2 * t + (s & 1);
+}
+
+// (tile, stage-in-tile, ring slot, phase) walked incrementally: no 64-bit
+// divisions in the pipelined loops.
+struct StageCursor {
+    long long tile, st;
+    int slot;
+    uint32_t ph;
+    __device__ __forceinline__ void init(long long lo, long long spt) {
+        tile = lo / spt;
+        st = lo - tile * spt;
+        slot = 0;
+        ph = 0;
+    }
+    template <int STAGES>
+    __device__ __forceinline__ void next(long long spt) {
+        if (++st == spt) {
+            st = 0;
+            ++tile;
+        }
+        if (++slot == STAGES) {
+            slot = 0;
+            ph ^= 1u;
+        }
+    }
+};
+
 template <int NB, int TAIL, bool KMAJ>
 __global__ void __launch_bounds__(kThreads, 1)
     mttkrp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcPlan p) {
     using Cfg = TcCfg<NB, TAIL>;
-    constexpr int CP = Cfg::CP;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // realign in the shared window (keeps the pointer in the shared state
+    // space so every fragment load compiles to LDS, not a generic LD)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = smem;
     double* sB = reinterpret_cast<double*>(smem + STAGES * Cfg::A_BYTES);
     double* sEpi = reinterpret_cast<double*>(smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES));
@@ -58,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1 + kBuilderWarps);
+            mbar_init(&full[s], 2);  // producer expect_tx + the stage's builder warp
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_barrier_init();
@@ -73,35 +107,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ producer
     if (warp == kConsumerWarps + kBuilderWarps) {
         if (lane == 0) {
-            long long it = 0;
-            for (long long gs = lo; gs < hi; ++gs, ++it) {
-                const int slot = static_cast<int>(it % STAGES);
-                const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
-                mbar_wait(&empty[slot], ph ^ 1u);
+            const uint64_t pol = l2_evict_first_policy();
+            StageCursor cur;
+            cur.init(lo, spt);
+            for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt)) {
+                const int slot = cur.slot;
+                const long long tile = cur.tile;
+                const long long st = cur.st;
+                mbar_wait(&empty[slot], cur.ph ^ 1u);
                 mbar_arrive_expect_tx(&full[slot], Cfg::A_BYTES);
-                const long long tile = gs / spt;
-                const long long st = gs - tile * spt;
                 unsigned char* dst = sA + slot * Cfg::A_BYTES;
                 if (!KMAJ) {
                     const int m0 = static_cast<int>(tile * kBM);
                     const int j0 = static_cast<int>(st * kBK);
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 4096, &tmap, &full[slot], m0 + 16 * b, j0);
+                    for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 4096, &tmap, &full[slot], m0 + 16 * b, j0, pol);
                 } else if (p.flavor == kKMajorJ) {
-                    const long long ti = tile % p.n_ti;
-                    const long long tj = tile / p.n_ti;
+                    const long long tj = div_nn(tile, p.n_ti);
+                    const long long ti = tile - tj * p.n_ti;
                     const int l0 = static_cast<int>(st * kBK);
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         tma_load_3d(dst + h * 16384, &tmap, &full[slot], l0 + 16 * h, static_cast<int>(ti * p.BI),
-                                    static_cast<int>(tj * p.BJ));
+                                    static_cast<int>(tj * p.BJ), pol);
                 } else {
-                    const long long j = st / p.n_lc;
+                    const long long j = div_nn(st, p.n_lc);
                     const long long lc = st - j * p.n_lc;
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         tma_load_3d(dst + h * 16384, &tmap, &full[slot], static_cast<int>(lc * kBK + 16 * h),
-                                    static_cast<int>(tile * kBM), static_cast<int>(j));
+                                    static_cast<int>(tile * kBM), static_cast<int>(j), pol);
                 }
             }
         }
@@ -109,79 +144,141 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ------------------------------------------------------------ builders
+    // Builder warp bw owns the stages it % kBuilderWarps == bw. Lane (g, t)
+    // produces exactly the B values DMMA lane (g, t) consumes: rows
+    // kperm(s, t) for the 8 k4-steps, columns nb*8 + g. All factor loads of a
+    // stage are issued before any is used (one L2 round trip per stage), and
+    // the stores are 128-bit, lane-contiguous (conflict-free).
     if (warp >= kConsumerWarps) {
-        const int tau = threadIdx.x - kConsumerWarps * 32;  // 0..63
-        const KrpGen& g = p.bgen;
-        const long long e0 = g.ext[0];
+        const int bw = warp - kConsumerWarps;
+        const int g = lane >> 2;
+        const int t = lane & 3;
+        const KrpGen& G = p.bgen;
+        const long long e0 = G.ext[0];
         const bool fast = e0 >= kBK;
-        long long it = 0;
-        for (long long gs = lo; gs < hi; ++gs, ++it) {
-            const int slot = static_cast<int>(it % STAGES);
-            const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
-            const long long tile = gs / spt;
-            const long long st = gs - tile * spt;
+        const int C = p.C;
+        StageCursor cur;
+        cur.init(lo, spt);
+        int mine = 0;
+        for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
+            if (mine != bw) continue;
+            const int slot = cur.slot;
+            const uint32_t ph = cur.ph;
+            const long long st = cur.st;
             long long kbase, jx = -1;
             if (KMAJ && p.flavor == kKMajorJK) {
-                jx = st / p.n_lc;
+                jx = div_nn(st, p.n_lc);
                 kbase = (st - jx * p.n_lc) * kBK;
             } else {
                 kbase = st * kBK;
             }
-            (void)tile;
-            mbar_wait(&empty[slot], ph ^ 1u);
-            const long long q0 = kbase / e0;
-            const int r0 = static_cast<int>(kbase - q0 * e0);
+            double u[8][NB];
+            double ut[8];
+            bool hsel[8];
+            double hv[2][NB];
+            double ht[2];
             if (fast) {
-                for (int e = tau; e < 2 * CP; e += 64) {
-                    const int h = e / CP;
-                    const int c = e - h * CP;
-                    double v = 0.0;
-                    if (c < p.C) {
-                        v = krp_head(g, (q0 + h) * e0, c);
-                        if (jx >= 0) v *= krp_value(p.sgen, jx, c);
+                const long long q0 = div_nn(kbase, e0);
+                const int r0 = static_cast<int>(kbase - q0 * e0);
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const int kr = kperm<KMAJ>(s, t);
+                    int r = r0 + kr;
+                    hsel[s] = r >= e0;
+                    if (hsel[s]) r -= static_cast<int>(e0);
+                    const bool valid = kbase + kr < p.kext;
+                    const double* row = G.U[0] + static_cast<long long>(r) * G.ldu;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) {
+                        const int c = nb * 8 + g;
+                        u[s][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
                     }
-                    sHead[h * CP + c] = v;
+                    ut[s] = 0.0;
+                    if (TAIL > 0) {
+                        const int c = 8 * NB + g;
+                        ut[s] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
+                    }
                 }
-                named_bar_sync(1, 64);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const long long idx = (q0 + h) * e0;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
+                    ht[h] = 1.0;
+                    for (int f = 1; f < G.nf; ++f) {
+                        const long long d = krp_digit(G, f, idx);
+                        const double* row = G.U[f] + d * G.ldu;
+#pragma unroll
+                        for (int nb = 0; nb < NB; ++nb) {
+                            const int c = nb * 8 + g;
+                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                        }
+                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                    }
+                    if (jx >= 0) {
+                        const KrpGen& S = p.sgen;
+                        for (int f = 0; f < S.nf; ++f) {
+                            const long long d = krp_digit(S, f, jx);
+                            const double* row = S.U[f] + d * S.ldu;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) {
+                                const int c = nb * 8 + g;
+                                hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                            }
+                            if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                        }
+                    }
+                }
+            } else {
+                // small fastest radix (< 32 rows): full product per entry
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const int kr = kperm<KMAJ>(s, t);
+                    const long long kidx = kbase + kr;
+                    const bool valid = kidx < p.kext;
+                    hsel[s] = false;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) {
+                        const int c = nb * 8 + g;
+                        double v = 0.0;
+                        if (valid && c < C) {
+                            v = krp_value(G, kidx, c);
+                            if (jx >= 0) v *= krp_value(p.sgen, jx, c);
+                        }
+                        u[s][nb] = v;
+                    }
+                    ut[s] = 0.0;
+                    if (TAIL > 0) {
+                        const int c = 8 * NB + g;
+                        if (valid && g < TAIL && c < C) {
+                            ut[s] = krp_value(G, kidx, c);
+                            if (jx >= 0) ut[s] *= krp_value(p.sgen, jx, c);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
+                ht[0] = ht[1] = 1.0;
             }
+            mbar_wait(&empty[slot], ph ^ 1u);
             double* Bm = sB + slot * (Cfg::B_BYTES / 8);
             double* Bt = Bm + Cfg::BMAIN;
-            const double* U0 = g.U[0];
-            for (int e = tau; e < kBK * CP; e += 64) {
-                const int kr = e / CP;
-                const int c = e - kr * CP;
-                const long long kidx = kbase + kr;
-                double v = 0.0;
-                if (kidx < p.kext && c < p.C) {
-                    if (fast) {
-                        int r = r0 + kr;
-                        int h = 0;
-                        if (r >= e0) {
-                            r -= static_cast<int>(e0);
-                            h = 1;
-                        }
-                        v = __ldg(U0 + static_cast<long long>(r) * g.ldu + c) * sHead[h * CP + c];
-                    } else {
-                        v = krp_value(g, kidx, c);
-                        if (jx >= 0) v *= krp_value(p.sgen, jx, c);
-                    }
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    double2 v;
+                    v.x = u[2 * s2][nb] * (hsel[2 * s2] ? hv[1][nb] : hv[0][nb]);
+                    v.y = u[2 * s2 + 1][nb] * (hsel[2 * s2 + 1] ? hv[1][nb] : hv[0][nb]);
+                    *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
                 }
-                // inverse of kperm: row kr -> (k4 step s, fragment lane column t)
-                const int rr = kr & 7;
-                const int s = ((kr >> 3) << 1) | ((rr >> 1) & 1);
-                const int rp = rr & ~2;
-                const int t = ((rp & 1) << 1) | (rp >> 2);
-                if (c < 8 * NB) {
-                    const int nb = c >> 3;
-                    const int gq = c & 7;
-                    Bm[((((s >> 1) * NB + nb) * 32 + gq * 4 + t) << 1) | (s & 1)] = v;
-                } else if (TAIL > 0) {
-                    Bt[(s * 4 + t) * (TAIL > 0 ? TAIL : 1) + (c - 8 * NB)] = v;
-                }
+            }
+            if (TAIL > 0 && g < TAIL) {
+#pragma unroll
+                for (int s = 0; s < 8; ++s) Bt[(s * 4 + t) * TAIL + g] = ut[s] * (hsel[s] ? ht[1] : ht[0]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
-            if (fast) named_bar_sync(1, 64);
         }
         return;
     }
@@ -190,24 +287,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int w = warp;
     const int gl = lane >> 2;  // fragment row / B column
     const int tl = lane & 3;   // fragment k / D column pair
-    const int kt = (tl >> 1) + 4 * (tl & 1);  // kperm lane term
-    // per-lane A offsets (bytes within the stage) for the two parities of s
-    // (and of rb for M-major / of (s>>1) for K-major)
-    uint32_t aoff[2][2];
+    // per-lane A fragment offsets (bytes within a stage), see kperm
+    uint32_t aoff[4];
 #pragma unroll
-    for (int x = 0; x < 2; ++x) {
-#pragma unroll
-        for (int y = 0; y < 2; ++y) {
-            if (!KMAJ) {
-                // x = s & 1, y = rb & 1 ; box-relative row k&7 = 2x + kt
-                const uint32_t kr7 = 2 * x + kt;
-                const uint32_t mm = 8 * y + gl;
-                aoff[x][y] = kr7 * 128 + ((mm * 8) ^ (kr7 << 4));
-            } else {
-                // x = (s >> 1) & 1, y = s & 1 ; kk = 8x + 2y + kt
-                const uint32_t kk = 8 * x + 2 * y + kt;
-                aoff[x][y] = (kk * 8) ^ (static_cast<uint32_t>(gl) << 4);
-            }
+    for (int x = 0; x < 4; ++x) {
+        if (!KMAJ) {
+            // x = 2 * (s & 1) + (rb & 1); box row k & 7 = 2 t + (s & 1)
+            const uint32_t kr7 = 2 * tl + (x >> 1);
+            const uint32_t mm = 8 * (x & 1) + gl;
+            aoff[x] = kr7 * 128 + ((mm * 8) ^ (kr7 << 4));
+        } else {
+            // x = s & 3; k & 15 = 8 (t >> 1) + (t & 1) + 2 (s & 3)
+            const uint32_t kk = 8 * (tl >> 1) + (tl & 1) + 2 * x;
+            aoff[x] = (kk * 8) ^ (static_cast<uint32_t>(gl) << 4);
         }
     }
 
@@ -223,12 +315,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     double* Pw = sEpi + w * 32 * Cfg::EPI_LD;
     int seg = 0;
-    long long it = 0;
-    for (long long gs = lo; gs < hi; ++gs, ++it) {
-        const int slot = static_cast<int>(it % STAGES);
-        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
-        const long long tile = gs / spt;
-        mbar_wait(&full[slot], ph);
+    StageCursor cur;
+    cur.init(lo, spt);
+    for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt)) {
+        const int slot = cur.slot;
+        const long long tile = cur.tile;
+        mbar_wait(&full[slot], cur.ph);
         const unsigned char* As = sA + slot * Cfg::A_BYTES;
         const double* Bm = sB + slot * (Cfg::B_BYTES / 8);
         const double* Bt = Bm + Cfg::BMAIN;
@@ -246,9 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int rb = 0; rb < 4; ++rb) {
                     uint32_t off;
                     if (!KMAJ) {
-                        off = (2 * w + (rb >> 1)) * 4096 + (s >> 1) * 1024 + aoff[s & 1][rb & 1];
+                        off = (2 * w + (rb >> 1)) * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
                     } else {
-                        off = (s >> 2) * 16384 + (32 * w + 8 * rb + gl) * 128 + aoff[(s >> 1) & 1][s & 1];
+                        off = (s >> 2) * 16384 + (32 * w + 8 * rb + gl) * 128 + aoff[s & 3];
                     }
                     a[rb] = *reinterpret_cast<const double*>(As + off);
                 }
@@ -273,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
 
-        const bool seg_end = (gs + 1 == hi) || ((gs + 1) / spt != tile);
+        const bool seg_end = (gs + 1 == hi) || (cur.st + 1 == spt);
         if (!seg_end) continue;
 
         // ------------------------------------------------- epilogue (warp-local)
@@ -307,18 +399,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.L == 1) {
                     for (int r = 0; r < 32 && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
                 } else if (mbase < mrows) {
-                    const long long ifirst = mbase / p.L;
+                    const long long ifirst = div_nn(mbase, p.L);
+                    long long l = mbase - ifirst * p.L;
                     long long cur = ifirst;
                     double sum = 0.0;
-                    for (int r = 0; r < 32 && mbase + r < mrows; ++r) {
-                        const long long m = mbase + r;
-                        const long long i = m / p.L;
-                        if (i != cur) {
+                    for (int r = 0; r < 32 && mbase + r < mrows; ++r, ++l) {
+                        if (l == p.L) {
                             wsb[(cur - ifirst) * C + c] = sum;
-                            cur = i;
+                            ++cur;
                             sum = 0.0;
+                            l = 0;
                         }
-                        sum += Pw[r * LD + c] * krp_value(p.sgen, m - i * p.L, c);
+                        sum += Pw[r * LD + c] * krp_value(p.sgen, l, c);
                     }
                     wsb[(cur - ifirst) * C + c] = sum;
                 }
