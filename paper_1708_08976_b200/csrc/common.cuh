@@ -47,6 +47,13 @@ __device__ __forceinline__ double krp_value(const KrpGen& g, long long idx, int 
     return v;
 }
 
+// krp_value with the single-factor case (a materialised or one-input KRP,
+// the common scale operand of the multi-TTV epilogue) as one plain load.
+__device__ __forceinline__ double krp_scale(const KrpGen& g, long long idx, int c) {
+    if (g.nf == 1) return __ldg(g.U[0] + idx * g.ldu + c);  // idx < ext for every caller
+    return krp_value(g, idx, c);
+}
+
 // Same, skipping factor 0 (the "head" partial product of the slower inputs).
 __device__ __forceinline__ double krp_head(const KrpGen& g, long long idx, int c) {
     double v = 1.0;

@@ -366,21 +366,21 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
         for (long long tile = t0; tile <= t1; ++tile) {
             const long long seg = tile - t0;
             for (int w = 0; w < kConsumerWarps; ++w) {
-                const long long base = (static_cast<long long>(b) * p.max_seg + seg) * kBM + 32 * w;
+                const long long base = (static_cast<long long>(b) * p.max_seg + seg) * kBM + kRowsPerWarp * w;
                 if (p.flavor == kMMajor) {
-                    const long long mrows = p.L * p.I, mbase = tile * kBM + 32 * w;
+                    const long long mrows = p.L * p.I, mbase = tile * kBM + kRowsPerWarp * w;
                     if (p.L == 1) {
-                        for (int r = 0; r < 32 && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
+                        for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
                     } else if (mbase < mrows) {
                         const long long ifirst = mbase / p.L;
-                        const long long ilast = std::min(mbase + 31, mrows - 1) / p.L;
+                        const long long ilast = std::min(mbase + kRowsPerWarp - 1, mrows - 1) / p.L;
                         for (long long i = ifirst; i <= ilast; ++i) out.push_back({i, base + (i - ifirst)});
                     }
                 } else if (p.flavor == kKMajorJ) {
                     const long long ti = tile % p.n_ti, tj = tile / p.n_ti;
-                    if (p.BI >= 32) {
-                        for (int r = 0; r < 32; ++r) {
-                            const int rho = 32 * w + r;
+                    if (p.BI >= kRowsPerWarp) {
+                        for (int r = 0; r < kRowsPerWarp; ++r) {
+                            const int rho = kRowsPerWarp * w + r;
                             const long long i = ti * p.BI + rho % p.BI, j = tj * p.BJ + rho / p.BI;
                             if (i < p.I && j < p.R) out.push_back({i, base + r});
                         }
@@ -391,8 +391,8 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
                         }
                     }
                 } else {
-                    const long long ibase = tile * kBM + 32 * w;
-                    for (int r = 0; r < 32 && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
+                    const long long ibase = tile * kBM + kRowsPerWarp * w;
+                    for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
                 }
             }
         }
@@ -590,6 +590,7 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         mp.tc.bgen = bgen;
         mp.tc.sgen = sgen;
         mp.tc.ws = ctx.ws.p;
+        if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
         const CUtensorMap map = make_map(X, mp);
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
             fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");

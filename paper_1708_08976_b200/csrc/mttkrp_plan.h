@@ -27,9 +27,11 @@
 
 namespace dmtkg {
 
-constexpr int kBM = 128;  // tile rows (4 consumer warps x 32)
+constexpr int kBM = 128;  // tile rows (8 consumer warps x 16)
 constexpr int kBK = 32;   // contraction depth per pipeline stage
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;   // two per SM sub-partition
+constexpr int kRowsPerWarp = kBM / kConsumerWarps;  // 16
+constexpr int kRB = kRowsPerWarp / 8;               // DMMA row blocks per warp
 constexpr int kBuilderWarps = 2;
 constexpr int kThreads = (kConsumerWarps + kBuilderWarps + 1) * 32;
 
@@ -46,6 +48,7 @@ struct TcPlan {
     long long total_stages;   // n_ti * n_tj * stages_per_tile
     long long kext;           // extent of the B generator index (R for M-major, L for K-major)
     int max_seg;              // workspace slot blocks per CTA
+    int debug;                // experiment switches (0 in production)
     KrpGen bgen;              // B operand rows (index j for M-major, l for K-major)
     KrpGen sgen;              // scale rows: KL over l (M-major), KR over j (K-major)
     double* ws;               // [grid][max_seg][128][C]

@@ -2,17 +2,19 @@
 // on-the-fly Khatri-Rao B tiles, FP64 tensor-core (DMMA 8x8x4) contraction,
 // fused multi-TTV epilogue. See mttkrp_plan.h for the formulation.
 //
-// Warp roles (224 threads, one CTA per SM, persistent over a stream-K range):
-//   warps 0-3  consumers: 32 tile rows each x all C columns. Columns in
+// Warp roles (352 threads, one CTA per SM, persistent over a stream-K range):
+//   warps 0-7  consumers (two per SM sub-partition, so one warp's loads and
+//              barrier waits hide behind the other's DMMAs): 16 tile rows
+//              each x all C columns. Columns in
 //              groups of 8 run on DMMA; the C % 8 remainder ("tail") runs on
 //              DFMA so no tensor-core work is wasted on padding.
-//   warps 4-5  builders, alternating stages: write the stage's B tile (32
+//   warps 8-9  builders, alternating stages: write the stage's B tile (32
 //              KRP rows x C) into shared memory in DMMA fragment order, one
 //              multiply per entry (cached head partial x fastest factor row:
 //              the paper's reuse scheme, Alg. 1, krp.cpp:53-88).
-//   warp 6     producer: one elected lane issues the TMA box loads.
+//   warp 10    producer: one elected lane issues the TMA box loads.
 // Per stage: full barrier (TMA bytes + 1 builder arrival), empty barrier
-// (4 consumer arrivals).
+// (8 consumer arrivals).
 //
 // The A tile arrives through 128-byte-swizzled TMA boxes; the k index a
 // DMMA fragment lane reads is permuted (kperm) so that all fragment loads
@@ -32,7 +34,7 @@ struct TcCfg {
     static constexpr int BTAIL = kBK * TAIL;    // doubles
     static constexpr int B_BYTES = ((BMAIN + BTAIL) * 8 + 1023) / 1024 * 1024;
     static constexpr int EPI_LD = CP + 1;
-    static constexpr int EPI_BYTES = ((kConsumerWarps * 32 * EPI_LD * 8) + 127) / 128 * 128;
+    static constexpr int EPI_BYTES = ((kConsumerWarps * kRowsPerWarp * EPI_LD * 8) + 127) / 128 * 128;
     static constexpr int HEAD_BYTES = 2 * 64 * 8;
     static constexpr int BAR_BYTES = 2 * STAGES * 8;
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + HEAD_BYTES + BAR_BYTES + 1024;
@@ -115,6 +117,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const long long tile = cur.tile;
                 const long long st = cur.st;
                 mbar_wait(&empty[slot], cur.ph ^ 1u);
+                if (p.debug & 2) {
+                    mbar_arrive(&full[slot]);
+                    continue;
+                }
                 mbar_arrive_expect_tx(&full[slot], Cfg::A_BYTES);
                 unsigned char* dst = sA + slot * Cfg::A_BYTES;
                 if (!KMAJ) {
@@ -157,11 +163,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long e0 = G.ext[0];
         const bool fast = e0 >= kBK;
         const int C = p.C;
+        const double* __restrict__ U0 = G.U[0];
+        const long long ldu = G.ldu;
+        const long long kext = p.kext;
+        // head partial products (all factors but the fastest, times KR(j)
+        // for the one-step flavor) change only every e0 rows: cached here
+        double hv[2][NB];
+        double ht[2];
+        long long hq = -1, hj = -2;
         StageCursor cur;
         cur.init(lo, spt);
         int mine = 0;
         for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
             if (mine != bw) continue;
+            if (p.debug & 1) {
+                mbar_wait(&empty[cur.slot], cur.ph ^ 1u);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[cur.slot]);
+                continue;
+            }
             const int slot = cur.slot;
             const uint32_t ph = cur.ph;
             const long long st = cur.st;
@@ -172,110 +192,124 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 kbase = st * kBK;
             }
-            double u[8][NB];
-            double ut[8];
-            bool hsel[8];
-            double hv[2][NB];
-            double ht[2];
+            // Loads of a chunk of k4-steps are all issued before use; for wide
+            // ranks the stage is built in two chunks to bound registers.
+            constexpr int NCH = NB > 4 ? 2 : 1;
+            constexpr int SPC = 8 / NCH;
+            long long q0 = 0;
+            int r0 = 0;
             if (fast) {
-                const long long q0 = div_nn(kbase, e0);
-                const int r0 = static_cast<int>(kbase - q0 * e0);
-#pragma unroll
-                for (int s = 0; s < 8; ++s) {
-                    const int kr = kperm<KMAJ>(s, t);
-                    int r = r0 + kr;
-                    hsel[s] = r >= e0;
-                    if (hsel[s]) r -= static_cast<int>(e0);
-                    const bool valid = kbase + kr < p.kext;
-                    const double* row = G.U[0] + static_cast<long long>(r) * G.ldu;
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) {
-                        const int c = nb * 8 + g;
-                        u[s][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
-                    }
-                    ut[s] = 0.0;
-                    if (TAIL > 0) {
-                        const int c = 8 * NB + g;
-                        ut[s] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const long long idx = (q0 + h) * e0;
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
-                    ht[h] = 1.0;
-                    for (int f = 1; f < G.nf; ++f) {
-                        const long long d = krp_digit(G, f, idx);
-                        const double* row = G.U[f] + d * G.ldu;
-#pragma unroll
-                        for (int nb = 0; nb < NB; ++nb) {
-                            const int c = nb * 8 + g;
-                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                        }
-                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                    }
-                    if (jx >= 0) {
-                        const KrpGen& S = p.sgen;
-                        for (int f = 0; f < S.nf; ++f) {
-                            const long long d = krp_digit(S, f, jx);
-                            const double* row = S.U[f] + d * S.ldu;
-#pragma unroll
-                            for (int nb = 0; nb < NB; ++nb) {
-                                const int c = nb * 8 + g;
-                                hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                            }
-                            if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                        }
-                    }
-                }
-            } else {
-                // small fastest radix (< 32 rows): full product per entry
-#pragma unroll
-                for (int s = 0; s < 8; ++s) {
-                    const int kr = kperm<KMAJ>(s, t);
-                    const long long kidx = kbase + kr;
-                    const bool valid = kidx < p.kext;
-                    hsel[s] = false;
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) {
-                        const int c = nb * 8 + g;
-                        double v = 0.0;
-                        if (valid && c < C) {
-                            v = krp_value(G, kidx, c);
-                            if (jx >= 0) v *= krp_value(p.sgen, jx, c);
-                        }
-                        u[s][nb] = v;
-                    }
-                    ut[s] = 0.0;
-                    if (TAIL > 0) {
-                        const int c = 8 * NB + g;
-                        if (valid && g < TAIL && c < C) {
-                            ut[s] = krp_value(G, kidx, c);
-                            if (jx >= 0) ut[s] *= krp_value(p.sgen, jx, c);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
-                ht[0] = ht[1] = 1.0;
+                q0 = div_nn(kbase, e0);
+                r0 = static_cast<int>(kbase - q0 * e0);
             }
-            mbar_wait(&empty[slot], ph ^ 1u);
             double* Bm = sB + slot * (Cfg::B_BYTES / 8);
             double* Bt = Bm + Cfg::BMAIN;
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
+            for (int ch = 0; ch < NCH; ++ch) {
+                double u[SPC][NB];
+                double ut[SPC];
+                bool hsel[SPC];
+                if (fast) {
 #pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
-                    double2 v;
-                    v.x = u[2 * s2][nb] * (hsel[2 * s2] ? hv[1][nb] : hv[0][nb]);
-                    v.y = u[2 * s2 + 1][nb] * (hsel[2 * s2 + 1] ? hv[1][nb] : hv[0][nb]);
-                    *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                    for (int ss = 0; ss < SPC; ++ss) {
+                        const int kr = kperm<KMAJ>(ch * SPC + ss, t);
+                        int r = r0 + kr;
+                        hsel[ss] = r >= e0;
+                        if (hsel[ss]) r -= static_cast<int>(e0);
+                        const bool valid = kbase + kr < kext;
+                        const double* row = U0 + r * ldu;
+#pragma unroll
+                        for (int nb = 0; nb < NB; ++nb) {
+                            const int c = nb * 8 + g;
+                            u[ss][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
+                        }
+                        ut[ss] = 0.0;
+                        if (TAIL > 0) {
+                            const int c = 8 * NB + g;
+                            ut[ss] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
+                        }
+                    }
+                    if (ch == 0 && (q0 != hq || jx != hj)) {
+                        hq = q0;
+                        hj = jx;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const long long idx = (q0 + h) * e0;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
+                            ht[h] = 1.0;
+                            for (int f = 1; f < G.nf; ++f) {
+                                const double* row = G.U[f] + krp_digit(G, f, idx) * G.ldu;
+#pragma unroll
+                                for (int nb = 0; nb < NB; ++nb) {
+                                    const int c = nb * 8 + g;
+                                    hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                                }
+                                if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                            }
+                            if (jx >= 0) {
+                                const KrpGen& S = p.sgen;
+                                for (int f = 0; f < S.nf; ++f) {
+                                    const double* row = S.U[f] + krp_digit(S, f, jx) * S.ldu;
+#pragma unroll
+                                    for (int nb = 0; nb < NB; ++nb) {
+                                        const int c = nb * 8 + g;
+                                        hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                                    }
+                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                }
+                            }
+                        }
+                    }
+                } else {
+                    // small fastest radix (< 32 rows): full product per entry
+                    hq = -1;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
+                    ht[0] = ht[1] = 1.0;
+#pragma unroll
+                    for (int ss = 0; ss < SPC; ++ss) {
+                        const int kr = kperm<KMAJ>(ch * SPC + ss, t);
+                        const long long kidx = kbase + kr;
+                        const bool valid = kidx < kext;
+                        hsel[ss] = false;
+#pragma unroll
+                        for (int nb = 0; nb < NB; ++nb) {
+                            const int c = nb * 8 + g;
+                            double v = 0.0;
+                            if (valid && c < C) {
+                                v = krp_value(G, kidx, c);
+                                if (jx >= 0) v *= krp_value(p.sgen, jx, c);
+                            }
+                            u[ss][nb] = v;
+                        }
+                        ut[ss] = 0.0;
+                        if (TAIL > 0) {
+                            const int c = 8 * NB + g;
+                            if (valid && g < TAIL && c < C) {
+                                ut[ss] = krp_value(G, kidx, c);
+                                if (jx >= 0) ut[ss] *= krp_value(p.sgen, jx, c);
+                            }
+                        }
+                    }
                 }
-            }
-            if (TAIL > 0 && g < TAIL) {
+                if (ch == 0) mbar_wait(&empty[slot], ph ^ 1u);
 #pragma unroll
-                for (int s = 0; s < 8; ++s) Bt[(s * 4 + t) * TAIL + g] = ut[s] * (hsel[s] ? ht[1] : ht[0]);
+                for (int sp = 0; sp < SPC / 2; ++sp) {
+                    const int s2 = ch * SPC / 2 + sp;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) {
+                        double2 v;
+                        v.x = u[2 * sp][nb] * (hsel[2 * sp] ? hv[1][nb] : hv[0][nb]);
+                        v.y = u[2 * sp + 1][nb] * (hsel[2 * sp + 1] ? hv[1][nb] : hv[0][nb]);
+                        *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                    }
+                }
+                if (TAIL > 0 && g < TAIL) {
+#pragma unroll
+                    for (int ss = 0; ss < SPC; ++ss)
+                        Bt[((ch * SPC + ss) * 4 + t) * TAIL + g] = ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
@@ -303,17 +337,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
-    double acc[4][NB][2];
-    double tacc[4][TAIL > 0 ? TAIL : 1];
+    double acc[kRB][NB][2];
+    double tacc[kRB][TAIL > 0 ? TAIL : 1];
 #pragma unroll
-    for (int rb = 0; rb < 4; ++rb) {
+    for (int rb = 0; rb < kRB; ++rb) {
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
 #pragma unroll
         for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) tacc[rb][tc] = 0.0;
     }
 
-    double* Pw = sEpi + w * 32 * Cfg::EPI_LD;
+    double* Pw = sEpi + w * kRowsPerWarp * Cfg::EPI_LD;
     int seg = 0;
     StageCursor cur;
     cur.init(lo, spt);
@@ -333,19 +367,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int sub = 0; sub < 2; ++sub) {
                 const int s = 2 * s2 + sub;
-                double a[4];
+                double a[kRB];
 #pragma unroll
-                for (int rb = 0; rb < 4; ++rb) {
+                for (int rb = 0; rb < kRB; ++rb) {
                     uint32_t off;
                     if (!KMAJ) {
-                        off = (2 * w + (rb >> 1)) * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
+                        off = (w * kRowsPerWarp / 16 + (rb >> 1)) * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
                     } else {
-                        off = (s >> 2) * 16384 + (32 * w + 8 * rb + gl) * 128 + aoff[s & 3];
+                        off = (s >> 2) * 16384 + (kRowsPerWarp * w + 8 * rb + gl) * 128 + aoff[s & 3];
                     }
                     a[rb] = *reinterpret_cast<const double*>(As + off);
                 }
 #pragma unroll
-                for (int rb = 0; rb < 4; ++rb) {
+                for (int rb = 0; rb < kRB; ++rb) {
 #pragma unroll
                     for (int nb = 0; nb < NB; ++nb)
                         dmma_8x8x4(acc[rb][nb][0], acc[rb][nb][1], a[rb], sub ? bv[nb].y : bv[nb].x);
@@ -355,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int tc = 0; tc < TAIL; ++tc) bt[tc] = Bt[(s * 4 + tl) * TAIL + tc];
 #pragma unroll
-                    for (int rb = 0; rb < 4; ++rb) {
+                    for (int rb = 0; rb < kRB; ++rb) {
 #pragma unroll
                         for (int tc = 0; tc < TAIL; ++tc) tacc[rb][tc] = fma(a[rb], bt[tc], tacc[rb][tc]);
                     }
@@ -371,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------- epilogue (warp-local)
         constexpr int LD = Cfg::EPI_LD;
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb) {
+        for (int rb = 0; rb < kRB; ++rb) {
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
                 Pw[(8 * rb + gl) * LD + 8 * nb + 2 * tl] = acc[rb][nb][0];
@@ -391,42 +425,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         const int C = p.C;
-        double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * kBM + 32 * w) * C;
+        double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * kBM + kRowsPerWarp * w) * C;
         for (int c = lane; c < C; c += 32) {
             if (!KMAJ) {
                 const long long mrows = p.L * p.I;
-                const long long mbase = tile * kBM + 32 * w;
+                const long long mbase = tile * kBM + kRowsPerWarp * w;
                 if (p.L == 1) {
-                    for (int r = 0; r < 32 && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
+                    for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
                 } else if (mbase < mrows) {
+                    // scale rows by KL(l, c): all loads issued before use
                     const long long ifirst = div_nn(mbase, p.L);
-                    long long l = mbase - ifirst * p.L;
+                    const long long l0 = mbase - ifirst * p.L;
+                    double sc[kRowsPerWarp];
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r) {
+                        long long l = l0 + r;
+                        if (l >= p.L) l -= p.L * div_nn(l, p.L);
+                        sc[r] = (mbase + r < mrows) ? krp_scale(p.sgen, l, c) : 0.0;
+                    }
+                    long long l = l0;
                     long long cur = ifirst;
                     double sum = 0.0;
-                    for (int r = 0; r < 32 && mbase + r < mrows; ++r, ++l) {
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r, ++l) {
+                        if (mbase + r >= mrows) break;
                         if (l == p.L) {
                             wsb[(cur - ifirst) * C + c] = sum;
                             ++cur;
                             sum = 0.0;
                             l = 0;
                         }
-                        sum += Pw[r * LD + c] * krp_value(p.sgen, l, c);
+                        sum += Pw[r * LD + c] * sc[r];
                     }
                     wsb[(cur - ifirst) * C + c] = sum;
                 }
             } else if (p.flavor == kKMajorJ) {
                 const long long ti = tile % p.n_ti;
                 const long long tj = tile / p.n_ti;
-                if (p.BI >= 32) {
-                    for (int r = 0; r < 32; ++r) {
-                        const int rho = 32 * w + r;
+                if (p.BI >= kRowsPerWarp) {
+                    double sc[kRowsPerWarp];
+                    bool ok[kRowsPerWarp];
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r) {
+                        const int rho = kRowsPerWarp * w + r;
                         const long long i = ti * p.BI + rho % p.BI;
                         const long long j = tj * p.BJ + rho / p.BI;
-                        if (i < p.I && j < p.R) wsb[r * C + c] = Pw[r * LD + c] * krp_value(p.sgen, j, c);
+                        ok[r] = i < p.I && j < p.R;
+                        sc[r] = ok[r] ? krp_scale(p.sgen, j, c) : 0.0;
                     }
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r)
+                        if (ok[r]) wsb[r * C + c] = Pw[r * LD + c] * sc[r];
                 } else {
-                    const int njl = 32 / p.BI;
-                    const int jl0 = (32 * w) / p.BI;
+                    const int njl = kRowsPerWarp / p.BI;
+                    const int jl0 = (kRowsPerWarp * w) / p.BI;
                     for (int il = 0; il < p.BI; ++il) {
                         const long long i = ti * p.BI + il;
                         if (i >= p.I) continue;
@@ -439,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                const long long ibase = tile * kBM + 32 * w;
-                for (int r = 0; r < 32 && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
+                const long long ibase = tile * kBM + kRowsPerWarp * w;
+                for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
             }
         }
         __syncwarp();
