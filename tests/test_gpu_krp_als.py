@@ -1,0 +1,168 @@
+"""GPU parity for the Khatri-Rao product and CP-ALS through the C ABI.
+
+KRP: bitwise equality with the Kronecker oracle (reference test_krp.cpp:69-91,
+krp.hpp:19-32) and the reference's KrpStats counts (test_krp.cpp:108-155).
+CP-ALS: reference test_cpals.cpp cases, plus fits within 1e-9 of the
+reference after the same number of iterations (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+import paper_1708_08976_b200 as dg
+from paper_1708_08976_b200 import AlsConfig, MttkrpAlgo as A
+
+pytestmark = pytest.mark.gpu
+
+
+def inputs(oracle, dims, cols, seed):
+    return [oracle.uniform(seed + z * 1000, d * cols).reshape(d, cols) for z, d in enumerate(dims)]
+
+
+@pytest.mark.parametrize("dims", [(6,), (3, 4), (2, 3, 4), (3, 2, 2, 3), (2, 2, 3, 2, 2), (4, 1, 3), (1, 1, 5),
+                                  (200, 200, 2), (5, 4, 3, 2)])
+@pytest.mark.parametrize("cols", [1, 3, 16, 25])
+def test_krp_bitwise(oracle, dims, cols):
+    ins = inputs(oracle, dims, cols, 42)
+    want = oracle.krp(ins)
+    assert np.array_equal(dg.krp(ins), want)
+    assert np.array_equal(dg.krp_naive(ins), want)
+
+
+def test_krp_known_answers():
+    a, b, c = np.array([[1.0, 2.0]]), np.array([[3.0, 4.0]]), np.array([[5.0, 6.0]])
+    assert dg.krp([a, b, c]).tolist() == [[15.0, 48.0]]
+    k = dg.krp([np.array([[1.0], [2.0]]), np.array([[3.0], [4.0]])])
+    assert k[:, 0].tolist() == [3.0, 4.0, 6.0, 8.0]
+    single = np.arange(15, dtype=float).reshape(5, 3)
+    assert np.array_equal(dg.krp([single]), single)
+
+
+def test_krp_stats_match_reference(ref, oracle):
+    for dims in [(2, 2, 2), (2, 2, 2, 2), (3, 4, 5), (5, 4, 3, 2), (2, 3, 2, 3, 2), (4, 4, 4, 4), (3, 2)]:
+        ins = inputs(oracle, dims, 3, 11)
+        s1, s2 = dg.KrpStats(), dg.KrpStats()
+        dg.krp(ins, 1, s1)
+        dg.krp_naive(ins, 1, s2)
+        _, want_reuse = ref.krp(ins, threads=1)
+        _, want_naive = ref.krp(ins, threads=1, naive=True)
+        assert s1.hadamard_products == want_reuse, dims
+        assert s2.hadamard_products == want_naive, dims
+
+
+def test_krp_validation():
+    with pytest.raises(dg.InvalidArgument):
+        dg.krp([])
+    with pytest.raises(dg.InvalidArgument):
+        dg.krp([np.ones((2, 2)), np.ones((2, 3))])
+    with pytest.raises(dg.InvalidArgument):
+        dg.krp([np.ones((2, 2)), None])
+
+
+def test_krp_config1_product(oracle):
+    """BASELINE config 1's 3-matrix KRP: 200x16 (.) 200x16 (.) 200x16 -> 8e6 x 16."""
+    ins = oracle.gen_factors((200, 200, 200), 16, 2)
+    got = dg.krp(ins)
+    # spot-check bitwise on rows through the oracle's small products
+    sub = oracle.krp([ins[0][:3], ins[1], ins[2]])
+    assert np.array_equal(got[:sub.shape[0]], sub)
+    r = 7_654_321
+    d0, d1, d2 = r // 40000, (r // 200) % 200, r % 200
+    assert np.array_equal(got[r], (ins[0][d0] * ins[1][d1]) * ins[2][d2])
+
+
+def cp(x, dims, rank, iters, seed, tol=0.0, algo=A.automatic):
+    t = dg.DenseTensor(dims, x)
+    return dg.cp_als(t, AlsConfig(rank=rank, max_iters=iters, tol=tol, seed=seed, algo=algo))
+
+
+@pytest.mark.parametrize("dims,rank,iters", [((6, 5, 4), 3, 6), ((7, 6, 5), 3, 8), ((8, 9, 10), 4, 40),
+                                             ((12, 10, 8, 6), 5, 10), ((40, 40, 12, 8), 20, 25)])
+def test_cp_als_fits_match_reference(ref, oracle, dims, rank, iters):
+    x = oracle.gen_tensor(dims, 31)
+    got = cp(x, dims, rank, iters, 7)
+    want = ref.cp_als(x, dims, rank, iters, tol=0.0, seed=7)
+    f_got = np.array([r.fit.fit for r in got.trace.iters])
+    assert len(f_got) == len(want["fits"])
+    assert np.max(np.abs(f_got - want["fits"])) <= 1e-9
+    assert abs(got.trace.tensor_norm - want["norm_x"]) <= 1e-12 * want["norm_x"]
+    for u in got.model.factors:  # final factors column-normalised (test_cpals.cpp:157-167)
+        assert np.allclose(np.linalg.norm(u, axis=0), 1.0, rtol=1e-12, atol=0)
+    assert np.all(got.model.lambda_ >= 0)
+
+
+def test_cp_als_monotone_and_deterministic(oracle):
+    dims = (8, 9, 10)
+    x = oracle.gen_tensor(dims, 77)
+    a = cp(x, dims, 4, 40, 13)
+    b = cp(x, dims, 4, 40, 13)
+    fa = [r.fit.fit for r in a.trace.iters]
+    assert len(fa) == 40
+    assert all(fa[i] >= fa[i - 1] - 1e-10 for i in range(1, 40))
+    assert fa == [r.fit.fit for r in b.trace.iters]
+    for u, v in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(u, v)
+
+
+def test_cp_als_rank1_recovery(oracle):
+    dims = (8, 7, 6)
+    f, lam = oracle.kruskal_random(dims, 1, 3)
+    x = oracle.reconstruct(f, lam)
+    res = cp(x, dims, 1, 30, 5)
+    assert res.trace.iters[-1].fit.fit >= 1 - 1e-6
+
+
+def test_cp_als_tolerance_stop_and_zero_tensor(oracle):
+    dims = (5, 5, 5)
+    x = oracle.gen_tensor(dims, 9)
+    assert len(cp(x, dims, 2, 50, 3, tol=1.0).trace.iters) == 2
+    assert len(cp(x, dims, 2, 12, 3, tol=0.0).trace.iters) == 12
+    z = cp(np.zeros(64), (4, 4, 4), 2, 10, 1)
+    assert z.trace.zero_tensor and z.trace.iters == [] and z.trace.tensor_norm == 0.0
+    assert all(np.all(u == 0) for u in z.model.factors) and np.all(z.model.lambda_ == 0)
+
+
+def test_cp_als_algorithms_agree(oracle):
+    dims = (6, 7, 8)
+    x = oracle.gen_tensor(dims, 50)
+    fits = [cp(x, dims, 3, 8, 4, algo=a).trace.iters[-1].fit.fit for a in (A.automatic, A.baseline, A.one_step)]
+    assert abs(fits[1] - fits[0]) <= 1e-8 and abs(fits[2] - fits[0]) <= 1e-8
+    with pytest.raises(dg.InvalidArgument):
+        cp(x, dims, 3, 8, 4, algo=A.two_step)
+
+
+def test_cp_als_validation(oracle):
+    x = oracle.gen_tensor((3, 3), 1)
+    for bad in (AlsConfig(rank=0), AlsConfig(rank=2, max_iters=-1), AlsConfig(rank=2, threads=0)):
+        with pytest.raises(dg.InvalidArgument):
+            dg.cp_als(dg.DenseTensor((3, 3), x), bad)
+
+
+def test_fit_matches_reference(ref, oracle):
+    dims = (6, 5, 4)
+    x = oracle.gen_tensor(dims, 31)
+    f, lam = oracle.kruskal_random(dims, 3, 7)
+    lam = np.array([2.0, 0.5, 1.0])
+    got = dg.fit(dg.DenseTensor(dims, x), dg.KruskalModel(f, lam))
+    want = ref.fit(x, dims, f, lam)
+    assert abs(got.fit - want["fit"]) <= 1e-10 and got.defined
+    with pytest.raises(dg.InvalidArgument):
+        dg.fit(dg.DenseTensor(dims, x), dg.KruskalModel(f[:2], lam))
+
+
+def test_gram_hadamard_and_solve(ref, oracle):
+    f, _ = oracle.kruskal_random((9, 8, 7), 5, 1)
+    for skip in (-1, 0, 1, 2):
+        assert np.allclose(dg.gram_hadamard(f, skip), ref.gram_hadamard(f, skip), rtol=1e-13, atol=0)
+    h = ref.gram_hadamard(f, 1)
+    m = oracle.uniform(3, 8 * 5).reshape(8, 5)
+    assert np.allclose(dg.solve_psd(h, m), ref.solve_psd(h, m), rtol=1e-9, atol=1e-12)
+    # singular H -> Jacobi pseudo-inverse path (test_linalg.cpp:239-298)
+    hs = np.ones((3, 3))
+    ms = np.array([[3.0, 3.0, 3.0], [1.0, 2.0, 3.0]])
+    assert np.allclose(dg.solve_psd(hs, ms), ref.solve_psd(hs, ms), rtol=1e-9, atol=1e-12)
+
+
+def test_tensor_norm(oracle, ref):
+    dims = (30, 20, 11)
+    x = oracle.gen_tensor(dims, 2)
+    assert abs(dg.tensor_norm(dg.DenseTensor(dims, x)) - ref.tensor_norm(x, dims)) <= 1e-13 * ref.tensor_norm(x, dims)
