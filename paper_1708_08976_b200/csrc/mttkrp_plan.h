@@ -32,8 +32,11 @@ constexpr int kBK = 32;   // contraction depth per pipeline stage
 constexpr int kConsumerWarps = 8;   // two per SM sub-partition
 constexpr int kRowsPerWarp = kBM / kConsumerWarps;  // 16
 constexpr int kRB = kRowsPerWarp / 8;               // DMMA row blocks per warp
-constexpr int kBuilderWarps = 2;
+constexpr int kBuilderWarps = 3;
 constexpr int kThreads = (kConsumerWarps + kBuilderWarps + 1) * 32;
+constexpr int kProducerWarp = 0;
+constexpr int kFirstBuilderWarp = 1;
+constexpr int kFirstConsumerWarp = 1 + kBuilderWarps;
 
 enum Flavor : int { kMMajor = 0, kKMajorJ = 1, kKMajorJK = 2 };
 
