@@ -125,7 +125,7 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
     std::recursive_mutex mu;
-    DevBuf ones, ws, fac, out, scratch, krp_scratch, reorder, als_small, norm_parts;
+    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts;
     int* flag = nullptr;
     Context() = default;
 };
@@ -268,17 +268,48 @@ static bool tail_of(int C, int& nb, int& tail) {
     return nb <= 8;
 }
 
-static void choose_kj_tiles(long long I, long long R, int& BI, int& BJ) {
-    long long best = -1;
-    for (int bi : {128, 64, 32, 16, 8, 4, 2, 1}) {
-        const int bj = 128 / bi;
-        const long long area = ((I + bi - 1) / bi) * bi * (((R + bj - 1) / bj) * bj);
-        if (best < 0 || area < best) {
-            best = area;
-            BI = bi;
-            BJ = bj;
+// Row-group count G (tile rows TR = 128 / G, each stage contracting 32 * G
+// indices split over the groups) and K-major row tile BI x BJ = TR, chosen to
+// minimise padded work: tile rows beyond the extent and contraction indices
+// beyond K are both zero-filled DMMA work. Smaller G wins near-ties (fewer B
+// rows to build per byte of X).
+struct Tiling {
+    int G, BI, BJ;
+};
+
+static double kwaste(long long K, int G) {
+    const long long step = 32LL * G;
+    return static_cast<double>(((K + step - 1) / step) * step) / static_cast<double>(K);
+}
+
+static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int max_g) {
+    Tiling best{1, 128, 1};
+    double best_cost = 1e300;
+    for (int G : {1, 2, 4}) {
+        if (G > max_g) break;
+        const int TR = kBM / G;
+        const double gpen = 1.0 + 0.02 * (G - 1);
+        if (flavor == kKMajorJ) {
+            for (int bi = TR; bi >= 1; bi /= 2) {
+                const int bj = TR / bi;
+                const double area = static_cast<double>(((rows_or_I + bi - 1) / bi) * bi) *
+                                    static_cast<double>(((R + bj - 1) / bj) * bj);
+                const double cost = area / (static_cast<double>(rows_or_I) * R) * kwaste(K, G) * gpen;
+                if (cost < best_cost - 1e-9) {
+                    best_cost = cost;
+                    best = {G, bi, bj};
+                }
+            }
+        } else {
+            const double pad = static_cast<double>(((rows_or_I + TR - 1) / TR) * TR) / static_cast<double>(rows_or_I);
+            const double cost = pad * kwaste(K, G) * gpen;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = {G, TR, 1};
+            }
         }
     }
+    return best;
 }
 
 // Flavor for (mode, resolved algorithm, order) on the collapsed view.
@@ -314,31 +345,56 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
     p.L = mp.L;
     p.I = mp.I;
     p.R = mp.R;
+    Tiling tl;
+    int max_g = 1;  // row groups whose B tiles still leave room for a 2-stage ring
+    for (int g : {2, 4})
+        if (tc_smem_bytes(mp.nb, mp.tail, g, 2) <= 227 * 1024) max_g = g;
     if (mp.kind == kTcM) {
         p.flavor = kMMajor;
-        p.n_ti = (mp.L * mp.I + kBM - 1) / kBM;
+        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, max_g);
+        p.G = tl.G;
+        p.TR = kBM / p.G;
+        p.n_ti = (mp.L * mp.I + p.TR - 1) / p.TR;
         p.n_tj = 1;
-        p.stages_per_tile = (mp.R + kBK - 1) / kBK;
+        p.stages_per_tile = (mp.R + kBK * p.G - 1) / (kBK * p.G);
         p.kext = mp.R;
-        p.BI = 128;
+        p.BI = p.TR;
         p.BJ = 1;
     } else if (mp.kind == kTcKJ) {
         p.flavor = kKMajorJ;
-        choose_kj_tiles(mp.I, mp.R, p.BI, p.BJ);
+        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, max_g);
+        p.G = tl.G;
+        p.TR = kBM / p.G;
+        p.BI = tl.BI;
+        p.BJ = tl.BJ;
         p.n_ti = (mp.I + p.BI - 1) / p.BI;
         p.n_tj = (mp.R + p.BJ - 1) / p.BJ;
-        p.stages_per_tile = (mp.L + kBK - 1) / kBK;
+        p.stages_per_tile = (mp.L + kBK * p.G - 1) / (kBK * p.G);
         p.kext = mp.L;
     } else {
         p.flavor = kKMajorJK;
-        p.BI = 128;
+        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, max_g);
+        p.G = tl.G;
+        p.TR = kBM / p.G;
+        p.BI = p.TR;
         p.BJ = 1;
-        p.n_ti = (mp.I + kBM - 1) / kBM;
+        p.n_ti = (mp.I + p.TR - 1) / p.TR;
         p.n_tj = 1;
-        p.n_lc = (mp.L + kBK - 1) / kBK;
+        p.n_lc = (mp.L + kBK * p.G - 1) / (kBK * p.G);
         p.stages_per_tile = mp.R * p.n_lc;
         p.kext = mp.L;
     }
+    // deepest ring (2..4 stages) that fits the 227 KB opt-in shared memory
+    p.stages = 0;
+    for (int st = 4; st >= 2; --st) {
+        const int sm = tc_smem_bytes(mp.nb, mp.tail, p.G, st);
+        if (sm > 0 && sm <= 227 * 1024) {
+            p.stages = st;
+            p.smem = sm;
+            break;
+        }
+    }
+    if (p.stages == 0) fail(DMTK_GPU_ERUNTIME, "mttkrp: no shared-memory configuration fits");
     mp.BI = p.BI;
     mp.BJ = p.BJ;
     p.total_stages = p.n_ti * p.n_tj * p.stages_per_tile;
@@ -358,6 +414,7 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
 // Host mirror of the kernel epilogue's slot assignment (mttkrp_tc.cuh):
 // (row i, workspace slot) pairs in (CTA, segment, warp, slot) order.
 static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long, long long>>& out) {
+    const int wpg = kConsumerWarps / p.G;
     for (int b = 0; b < grid; ++b) {
         long long lo, hi;
         cta_stage_range(p.total_stages, grid, b, lo, hi);
@@ -366,9 +423,10 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
         for (long long tile = t0; tile <= t1; ++tile) {
             const long long seg = tile - t0;
             for (int w = 0; w < kConsumerWarps; ++w) {
+                const int lw = w % wpg;  // every row group writes its own slots
                 const long long base = (static_cast<long long>(b) * p.max_seg + seg) * kBM + kRowsPerWarp * w;
                 if (p.flavor == kMMajor) {
-                    const long long mrows = p.L * p.I, mbase = tile * kBM + kRowsPerWarp * w;
+                    const long long mrows = p.L * p.I, mbase = tile * p.TR + kRowsPerWarp * lw;
                     if (p.L == 1) {
                         for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
                     } else if (mbase < mrows) {
@@ -380,7 +438,7 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
                     const long long ti = tile % p.n_ti, tj = tile / p.n_ti;
                     if (p.BI >= kRowsPerWarp) {
                         for (int r = 0; r < kRowsPerWarp; ++r) {
-                            const int rho = kRowsPerWarp * w + r;
+                            const int rho = kRowsPerWarp * lw + r;
                             const long long i = ti * p.BI + rho % p.BI, j = tj * p.BJ + rho / p.BI;
                             if (i < p.I && j < p.R) out.push_back({i, base + r});
                         }
@@ -391,7 +449,7 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
                         }
                     }
                 } else {
-                    const long long ibase = tile * kBM + kRowsPerWarp * w;
+                    const long long ibase = tile * p.TR + kRowsPerWarp * lw;
                     for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
                 }
             }
@@ -595,6 +653,25 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         mp.tc.bgen = bgen;
         mp.tc.sgen = sgen;
         mp.tc.ws = ctx.ws.p;
+        // heads = KRP of every B factor but the fastest (the reuse partial of
+        // krp.cpp:53-88), materialised once so a builder's head is one row load
+        mp.tc.htab = nullptr;
+        mp.tc.hrows = 0;
+        if (bgen.nf >= 2 && bgen.ext[0] >= kBK && bgen.ldu > 0) {
+            std::vector<const double*> in;
+            std::vector<long long> rows;
+            long long hr = 1;
+            for (int f = bgen.nf - 1; f >= 1; --f) {
+                in.push_back(bgen.U[f]);
+                rows.push_back(bgen.ext[f]);
+                hr *= bgen.ext[f];
+            }
+            ctx.htab.ensure(static_cast<size_t>(hr * C));
+            krp_materialize(in, rows, C, ctx.htab.p, ctx.scratch2, s);
+            mp.tc.htab = ctx.htab.p;
+            mp.tc.hrows = hr;
+        }
+
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
         const CUtensorMap map = make_map(X, mp);
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))

@@ -27,7 +27,7 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
 
 // Tensor-core streaming MTTKRP (mttkrp_tc.cuh). nb in [1, 8], tail in
 // {0, 1, 2, 4}; returns false when no instantiation matches.
-int tc_smem_bytes(int nb, int tail);
+int tc_smem_bytes(int nb, int tail, int G, int stages);
 bool launch_mttkrp_tc(const TcPlan& p, const CUtensorMap& map, int nb, int tail, bool kmajor, int grid, cudaStream_t s);
 
 }  // namespace dmtkg

@@ -27,7 +27,7 @@
 
 namespace dmtkg {
 
-constexpr int kBM = 128;  // tile rows (8 consumer warps x 16)
+constexpr int kBM = 128;  // rows per CTA tile stage (8 consumer warps x 16)
 constexpr int kBK = 32;   // contraction depth per pipeline stage
 constexpr int kConsumerWarps = 8;   // two per SM sub-partition
 constexpr int kRowsPerWarp = kBM / kConsumerWarps;  // 16
@@ -44,10 +44,14 @@ struct TcPlan {
     int flavor;
     int C;                    // rank
     long long L, I, R;        // collapsed view
-    int BI, BJ;               // K-major row tile: BI * BJ == 128 (kKMajorJK: 128, 1)
-    long long n_ti, n_tj;     // tiles along rows (M-major: n_ti = ceil(L*I/128), n_tj = 1)
-    long long stages_per_tile;  // contraction stages per tile
-    long long n_lc;           // kKMajorJK: l-chunks per j
+    int G;                    // row groups: the 128 tile rows are G groups of TR = 128/G rows,
+                              // each group contracting its own 32-index slice of a stage
+    int TR;                   // tile rows (128 / G)
+    int stages;               // ring depth (2..4)
+    int BI, BJ;               // K-major row tile: BI * BJ == TR (kKMajorJK: TR, 1)
+    long long n_ti, n_tj;     // tiles along rows (M-major: n_ti = ceil(L*I/TR), n_tj = 1)
+    long long stages_per_tile;  // contraction stages per tile (32 * G indices each)
+    long long n_lc;           // kKMajorJK: l-chunks of 32 * G per j
     long long total_stages;   // n_ti * n_tj * stages_per_tile
     long long kext;           // extent of the B generator index (R for M-major, L for K-major)
     int max_seg;              // workspace slot blocks per CTA
@@ -55,6 +59,9 @@ struct TcPlan {
     KrpGen bgen;              // B operand rows (index j for M-major, l for K-major)
     KrpGen sgen;              // scale rows: KL over l (M-major), KR over j (K-major)
     double* ws;               // [grid][max_seg][128][C]
+    const double* htab;       // partial KRP of bgen factors 1..nf-1 (hrows x C), or null
+    long long hrows;
+    int smem;                 // dynamic shared memory bytes
 };
 
 // Stage range of CTA b under the stream-K split.

@@ -30,16 +30,16 @@ namespace dmtkg {
 template <int NB, int TAIL>
 struct TcCfg {
     static constexpr int CP = 8 * NB + TAIL;
-    static constexpr int STAGES = NB <= 4 ? 4 : 3;
-    static constexpr int A_BYTES = kBM * kBK * 8;
-    static constexpr int BMAIN = kBK * 8 * NB;  // doubles
-    static constexpr int BTAIL = kBK * TAIL;    // doubles
-    static constexpr int B_BYTES = ((BMAIN + BTAIL) * 8 + 1023) / 1024 * 1024;
+    static constexpr int MAX_STAGES = 4;
+    static constexpr int A_BYTES = kBM * kBK * 8;  // one stage of X: 32 KB
+    static constexpr int BMAIN = kBK * 8 * NB;     // doubles per group, DMMA fragments
+    static constexpr int BTAIL = kBK * TAIL;       // doubles per group, DFMA tail columns
+    static constexpr int B_BYTES = ((BMAIN + BTAIL) * 8 + 1023) / 1024 * 1024;  // one row group
     static constexpr int EPI_LD = CP + 1;
-    static constexpr int EPI_BYTES = ((kConsumerWarps * kRowsPerWarp * EPI_LD * 8) + 127) / 128 * 128;
-    static constexpr int HEAD_BYTES = 2 * 64 * 8;
-    static constexpr int BAR_BYTES = 2 * STAGES * 8;
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + EPI_BYTES + HEAD_BYTES + BAR_BYTES + 1024;
+    static constexpr int EPI_BYTES = ((kConsumerWarps * kRowsPerWarp * EPI_LD * 8) + 1023) / 1024 * 1024;
+    static constexpr int BAR_BYTES = 2 * MAX_STAGES * 8;
+    // everything but the ring; the host adds stages * (A_BYTES + G * B_BYTES)
+    static constexpr int FIXED = EPI_BYTES + BAR_BYTES + 1024;
 };
 
 // Which contraction row of a 32-row stage DMMA lane column t reads at k4-step
@@ -63,13 +63,12 @@ struct StageCursor {
         slot = 0;
         ph = 0;
     }
-    template <int STAGES>
-    __device__ __forceinline__ void next(long long spt) {
+    __device__ __forceinline__ void next(long long spt, int stages) {
         if (++st == spt) {
             st = 0;
             ++tile;
         }
-        if (++slot == STAGES) {
+        if (++slot == stages) {
             slot = 0;
             ph ^= 1u;
         }
@@ -80,17 +79,18 @@ template <int NB, int TAIL, bool KMAJ>
 __global__ void __launch_bounds__(kThreads, 1)
     mttkrp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcPlan p) {
     using Cfg = TcCfg<NB, TAIL>;
-    constexpr int STAGES = Cfg::STAGES;
+    const int STAGES = p.stages;
+    const int G = p.G;
+    const int GB_BYTES = G * Cfg::B_BYTES;  // B tile of one stage (all row groups)
     extern __shared__ unsigned char smem_raw[];
     // realign in the shared window (keeps the pointer in the shared state
     // space so every fragment load compiles to LDS, not a generic LD)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = smem;
-    double* sB = reinterpret_cast<double*>(smem + STAGES * Cfg::A_BYTES);
-    double* sEpi = reinterpret_cast<double*>(smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES));
-    double* sHead = reinterpret_cast<double*>(smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES) + Cfg::EPI_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sHead) + Cfg::HEAD_BYTES);
-    uint64_t* empty = full + STAGES;
+    unsigned char* sB = smem + STAGES * Cfg::A_BYTES;
+    double* sEpi = reinterpret_cast<double*>(sB + STAGES * GB_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sEpi) + Cfg::EPI_BYTES);
+    uint64_t* empty = full + Cfg::MAX_STAGES;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol = l2_evict_first_policy();
             StageCursor cur;
             cur.init(lo, spt);
-            for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt)) {
+            for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
                 const int slot = cur.slot;
                 const long long tile = cur.tile;
                 const long long st = cur.st;
@@ -125,194 +125,220 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mbar_arrive_expect_tx(&full[slot], Cfg::A_BYTES);
                 unsigned char* dst = sA + slot * Cfg::A_BYTES;
+                const int gshift = 4 - __ffs(G);  // log2(8 / G): consumer warps (and 16-row boxes) per group
                 if (!KMAJ) {
-                    const int m0 = static_cast<int>(tile * kBM);
-                    const int j0 = static_cast<int>(st * kBK);
+                    // 8 boxes {16 m, 32 j}: box b is row group b >> gshift,
+                    // rows 16 * (b & (8/G - 1)) of the group's TR-row tile
+                    const int m0 = static_cast<int>(tile * p.TR);
+                    const int j0 = static_cast<int>(st * kBK * G);
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 4096, &tmap, &full[slot], m0 + 16 * b, j0, pol);
-                } else if (p.flavor == kKMajorJ) {
-                    const long long tj = div_nn(tile, p.n_ti);
-                    const long long ti = tile - tj * p.n_ti;
-                    const int l0 = static_cast<int>(st * kBK);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        tma_load_3d(dst + h * 16384, &tmap, &full[slot], l0 + 16 * h, static_cast<int>(ti * p.BI),
-                                    static_cast<int>(tj * p.BJ), pol);
+                    for (int b = 0; b < 8; ++b)
+                        tma_load_2d(dst + b * 4096, &tmap, &full[slot], m0 + 16 * (b & ((1 << gshift) - 1)),
+                                    j0 + kBK * (b >> gshift), pol);
                 } else {
-                    const long long j = div_nn(st, p.n_lc);
-                    const long long lc = st - j * p.n_lc;
+                    long long ti, tj, j, l0;
+                    if (p.flavor == kKMajorJ) {
+                        tj = div_nn(tile, p.n_ti);
+                        ti = tile - tj * p.n_ti;
+                        l0 = st * kBK * G;
+                        j = tj * p.BJ;
+                    } else {
+                        ti = tile;
+                        j = div_nn(st, p.n_lc);
+                        l0 = (st - j * p.n_lc) * kBK * G;
+                    }
+                    const int gbytes = Cfg::A_BYTES / G;
+                    for (int gi = 0; gi < G; ++gi) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        tma_load_3d(dst + h * 16384, &tmap, &full[slot], static_cast<int>(lc * kBK + 16 * h),
-                                    static_cast<int>(tile * kBM), static_cast<int>(j), pol);
+                            for (int h = 0; h < 2; ++h)
+                                tma_load_3d(dst + gi * gbytes + h * (gbytes / 2), &tmap, &full[slot],
+                                            static_cast<int>(l0 + kBK * gi + 16 * h), static_cast<int>(ti * p.BI),
+                                            static_cast<int>(j), pol);
+                        }
+                    }
                 }
             }
+            return;
         }
-        return;
-    }
 
-    // ------------------------------------------------------------ builders
-    // Builder warp bw owns the stages it % kBuilderWarps == bw. Lane (g, t)
-    // produces exactly the B values DMMA lane (g, t) consumes: rows
-    // kperm(s, t) for the 8 k4-steps, columns nb*8 + g. All factor loads of a
-    // stage are issued before any is used (one L2 round trip per stage), and
-    // the stores are 128-bit, lane-contiguous (conflict-free).
-    if (warp < kFirstConsumerWarp) {
-        const int bw = warp - kFirstBuilderWarp;
-        const int g = lane >> 2;
-        const int t = lane & 3;
-        const KrpGen& G = p.bgen;
-        const long long e0 = G.ext[0];
-        const bool fast = e0 >= kBK;
-        const int C = p.C;
-        const double* __restrict__ U0 = G.U[0];
-        const long long ldu = G.ldu;
-        const long long kext = p.kext;
-        // head partial products (all factors but the fastest, times KR(j)
-        // for the one-step flavor) change only every e0 rows: cached here
-        double hv[2][NB];
-        double ht[2];
-        long long hq = -1, hj = -2;
-        StageCursor cur;
-        cur.init(lo, spt);
-        int mine = 0;
-        for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
-            if (mine != bw) continue;
-            if (p.debug & 1) {
-                mbar_wait(&empty[cur.slot], cur.ph ^ 1u);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[cur.slot]);
-                continue;
-            }
-            const int slot = cur.slot;
-            const uint32_t ph = cur.ph;
-            const long long st = cur.st;
-            long long kbase, jx = -1;
-            if (KMAJ && p.flavor == kKMajorJK) {
-                jx = div_nn(st, p.n_lc);
-                kbase = (st - jx * p.n_lc) * kBK;
-            } else {
-                kbase = st * kBK;
-            }
-            // Loads of a chunk of k4-steps are all issued before use; for wide
-            // ranks the stage is built in two chunks to bound registers.
-            constexpr int NCH = NB > 4 ? 2 : 1;
-            constexpr int SPC = 8 / NCH;
-            long long q0 = 0;
-            int r0 = 0;
-            if (fast) {
-                q0 = div_nn(kbase, e0);
-                r0 = static_cast<int>(kbase - q0 * e0);
-            }
-            double* Bm = sB + slot * (Cfg::B_BYTES / 8);
-            double* Bt = Bm + Cfg::BMAIN;
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-                double u[SPC][NB];
-                double ut[SPC];
-                bool hsel[SPC];
-                if (fast) {
-#pragma unroll
-                    for (int ss = 0; ss < SPC; ++ss) {
-                        const int kr = kperm<KMAJ>(ch * SPC + ss, t);
-                        int r = r0 + kr;
-                        hsel[ss] = r >= e0;
-                        if (hsel[ss]) r -= static_cast<int>(e0);
-                        const bool valid = kbase + kr < kext;
-                        const double* row = U0 + r * ldu;
-#pragma unroll
-                        for (int nb = 0; nb < NB; ++nb) {
-                            const int c = nb * 8 + g;
-                            u[ss][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
-                        }
-                        ut[ss] = 0.0;
-                        if (TAIL > 0) {
-                            const int c = 8 * NB + g;
-                            ut[ss] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
-                        }
-                    }
-                    if (ch == 0 && (q0 != hq || jx != hj)) {
-                        hq = q0;
-                        hj = jx;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const long long idx = (q0 + h) * e0;
-#pragma unroll
-                            for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
-                            ht[h] = 1.0;
-                            for (int f = 1; f < G.nf; ++f) {
-                                const double* row = G.U[f] + krp_digit(G, f, idx) * G.ldu;
-#pragma unroll
-                                for (int nb = 0; nb < NB; ++nb) {
-                                    const int c = nb * 8 + g;
-                                    hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                                }
-                                if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                            }
-                            if (jx >= 0) {
-                                const KrpGen& S = p.sgen;
-                                for (int f = 0; f < S.nf; ++f) {
-                                    const double* row = S.U[f] + krp_digit(S, f, jx) * S.ldu;
-#pragma unroll
-                                    for (int nb = 0; nb < NB; ++nb) {
-                                        const int c = nb * 8 + g;
-                                        hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                                    }
-                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                                }
-                            }
-                        }
-                    }
+        // ------------------------------------------------------------ builders
+        // Builder warp bw owns the stages it % kBuilderWarps == bw. Lane (g, t)
+        // produces exactly the B values DMMA lane (g, t) consumes: rows
+        // kperm(s, t) for the 8 k4-steps, columns nb*8 + g. All factor loads of a
+        // stage are issued before any is used (one L2 round trip per stage), and
+        // the stores are 128-bit, lane-contiguous (conflict-free).
+        if (warp < kFirstConsumerWarp) {
+            const int bw = warp - kFirstBuilderWarp;
+            const int g = lane >> 2;
+            const int t = lane & 3;
+            const KrpGen& Gen = p.bgen;
+            const long long e0 = Gen.ext[0];
+            const bool fast = e0 >= kBK;
+            const int C = p.C;
+            const double* __restrict__ U0 = Gen.U[0];
+            const long long ldu = Gen.ldu;
+            const long long kext = p.kext;
+            // head partial products (all factors but the fastest, times KR(j)
+            // for the one-step flavor) change only every e0 rows: cached here
+            double hv[2][NB];
+            double ht[2];
+            long long hq = -1, hj = -2;
+            StageCursor cur;
+            cur.init(lo, spt);
+            int mine = 0;
+            for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
+                if (mine != bw) continue;
+                if (p.debug & 1) {
+                    mbar_wait(&empty[cur.slot], cur.ph ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[cur.slot]);
+                    continue;
+                }
+                const int slot = cur.slot;
+                const uint32_t ph = cur.ph;
+                const long long st = cur.st;
+                long long kstage, jx = -1;
+                if (KMAJ && p.flavor == kKMajorJK) {
+                    jx = div_nn(st, p.n_lc);
+                    kstage = (st - jx * p.n_lc) * kBK * G;
                 } else {
-                    // small fastest radix (< 32 rows): full product per entry
-                    hq = -1;
+                    kstage = st * kBK * G;
+                }
+                for (int gi = 0; gi < G; ++gi) {
+                const long long kbase = kstage + kBK * gi;
+                // Loads of a chunk of k4-steps are all issued before use; for wide
+                // ranks the stage is built in two chunks to bound registers.
+                constexpr int NCH = NB > 4 ? 2 : 1;
+                constexpr int SPC = 8 / NCH;
+                long long q0 = 0;
+                int r0 = 0;
+                if (fast) {
+                    q0 = div_nn(kbase, e0);
+                    r0 = static_cast<int>(kbase - q0 * e0);
+                }
+                double* Bm = reinterpret_cast<double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
+                double* Bt = Bm + Cfg::BMAIN;
 #pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
-                    ht[0] = ht[1] = 1.0;
+                for (int ch = 0; ch < NCH; ++ch) {
+                    double u[SPC][NB];
+                    double ut[SPC];
+                    bool hsel[SPC];
+                    if (fast) {
 #pragma unroll
-                    for (int ss = 0; ss < SPC; ++ss) {
-                        const int kr = kperm<KMAJ>(ch * SPC + ss, t);
-                        const long long kidx = kbase + kr;
-                        const bool valid = kidx < kext;
-                        hsel[ss] = false;
+                        for (int ss = 0; ss < SPC; ++ss) {
+                            const int kr = kperm<KMAJ>(ch * SPC + ss, t);
+                            int r = r0 + kr;
+                            hsel[ss] = r >= e0;
+                            if (hsel[ss]) r -= static_cast<int>(e0);
+                            const bool valid = kbase + kr < kext;
+                            const double* row = U0 + r * ldu;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) {
+                                const int c = nb * 8 + g;
+                                u[ss][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
+                            }
+                            ut[ss] = 0.0;
+                            if (TAIL > 0) {
+                                const int c = 8 * NB + g;
+                                ut[ss] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
+                            }
+                        }
+                        if (ch == 0 && (q0 != hq || jx != hj)) {
+                            hq = q0;
+                            hj = jx;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const long long idx = (q0 + h) * e0;
+#pragma unroll
+                                for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
+                                ht[h] = 1.0;
+                                if (p.htab) {
+                                    // materialised partial KRP of the slower factors: one row
+                                    if (q0 + h < p.hrows) {
+                                        const double* row = p.htab + (q0 + h) * C;
+#pragma unroll
+                                        for (int nb = 0; nb < NB; ++nb) {
+                                            const int c = nb * 8 + g;
+                                            hv[h][nb] = c < C ? __ldg(row + c) : 0.0;
+                                        }
+                                        if (TAIL > 0) ht[h] = (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    }
+                                } else {
+                                    for (int f = 1; f < Gen.nf; ++f) {
+                                        const double* row = Gen.U[f] + krp_digit(Gen, f, idx) * Gen.ldu;
+#pragma unroll
+                                        for (int nb = 0; nb < NB; ++nb) {
+                                            const int c = nb * 8 + g;
+                                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                                        }
+                                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    }
+                                }
+                                if (jx >= 0) {
+                                    const KrpGen& S = p.sgen;
+                                    for (int f = 0; f < S.nf; ++f) {
+                                        const double* row = S.U[f] + krp_digit(S, f, jx) * S.ldu;
+#pragma unroll
+                                        for (int nb = 0; nb < NB; ++nb) {
+                                            const int c = nb * 8 + g;
+                                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
+                                        }
+                                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    }
+                                }
+                            }
+                        }
+                    } else {
+                        // small fastest radix (< 32 rows): full product per entry
+                        hq = -1;
+#pragma unroll
+                        for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
+                        ht[0] = ht[1] = 1.0;
+#pragma unroll
+                        for (int ss = 0; ss < SPC; ++ss) {
+                            const int kr = kperm<KMAJ>(ch * SPC + ss, t);
+                            const long long kidx = kbase + kr;
+                            const bool valid = kidx < kext;
+                            hsel[ss] = false;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) {
+                                const int c = nb * 8 + g;
+                                double v = 0.0;
+                                if (valid && c < C) {
+                                    v = krp_value(Gen, kidx, c);
+                                    if (jx >= 0) v *= krp_value(p.sgen, jx, c);
+                                }
+                                u[ss][nb] = v;
+                            }
+                            ut[ss] = 0.0;
+                            if (TAIL > 0) {
+                                const int c = 8 * NB + g;
+                                if (valid && g < TAIL && c < C) {
+                                    ut[ss] = krp_value(Gen, kidx, c);
+                                    if (jx >= 0) ut[ss] *= krp_value(p.sgen, jx, c);
+                                }
+                            }
+                        }
+                    }
+                    if (gi == 0 && ch == 0) mbar_wait(&empty[slot], ph ^ 1u);
+#pragma unroll
+                    for (int sp = 0; sp < SPC / 2; ++sp) {
+                        const int s2 = ch * SPC / 2 + sp;
 #pragma unroll
                         for (int nb = 0; nb < NB; ++nb) {
-                            const int c = nb * 8 + g;
-                            double v = 0.0;
-                            if (valid && c < C) {
-                                v = krp_value(G, kidx, c);
-                                if (jx >= 0) v *= krp_value(p.sgen, jx, c);
-                            }
-                            u[ss][nb] = v;
-                        }
-                        ut[ss] = 0.0;
-                        if (TAIL > 0) {
-                            const int c = 8 * NB + g;
-                            if (valid && g < TAIL && c < C) {
-                                ut[ss] = krp_value(G, kidx, c);
-                                if (jx >= 0) ut[ss] *= krp_value(p.sgen, jx, c);
-                            }
+                            double2 v;
+                            v.x = u[2 * sp][nb] * (hsel[2 * sp] ? hv[1][nb] : hv[0][nb]);
+                            v.y = u[2 * sp + 1][nb] * (hsel[2 * sp + 1] ? hv[1][nb] : hv[0][nb]);
+                            *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
                         }
                     }
-                }
-                if (ch == 0) mbar_wait(&empty[slot], ph ^ 1u);
+                    if (TAIL > 0 && g < TAIL) {
 #pragma unroll
-                for (int sp = 0; sp < SPC / 2; ++sp) {
-                    const int s2 = ch * SPC / 2 + sp;
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) {
-                        double2 v;
-                        v.x = u[2 * sp][nb] * (hsel[2 * sp] ? hv[1][nb] : hv[0][nb]);
-                        v.y = u[2 * sp + 1][nb] * (hsel[2 * sp + 1] ? hv[1][nb] : hv[0][nb]);
-                        *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                        for (int ss = 0; ss < SPC; ++ss)
+                            Bt[((ch * SPC + ss) * 4 + t) * TAIL + g] = ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
                     }
                 }
-                if (TAIL > 0 && g < TAIL) {
-#pragma unroll
-                    for (int ss = 0; ss < SPC; ++ss)
-                        Bt[((ch * SPC + ss) * 4 + t) * TAIL + g] = ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
-                }
-            }
+            }  // row groups
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
         }
@@ -321,6 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ------------------------------------------------------------ consumers
     const int w = warp - kFirstConsumerWarp;
+    const int wpg = kConsumerWarps / G;  // consumer warps per row group
+    const int gi = w / wpg;              // this warp's row group (its contraction slice)
+    const int lw = w - gi * wpg;         // warp within the group: rows 16 lw .. 16 lw + 15
     const int gl = lane >> 2;  // fragment row / B column
     const int tl = lane & 3;   // fragment k / D column pair
     // per-lane A fragment offsets (bytes within a stage), see kperm
@@ -353,12 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int seg = 0;
     StageCursor cur;
     cur.init(lo, spt);
-    for (long long gs = lo; gs < hi; ++gs, cur.next<STAGES>(spt)) {
+    for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
         const int slot = cur.slot;
         const long long tile = cur.tile;
         mbar_wait(&full[slot], cur.ph);
         const unsigned char* As = sA + slot * Cfg::A_BYTES;
-        const double* Bm = sB + slot * (Cfg::B_BYTES / 8);
+        const double* Bm = reinterpret_cast<const double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
         const double* Bt = Bm + Cfg::BMAIN;
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) {
@@ -374,9 +403,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int rb = 0; rb < kRB; ++rb) {
                     uint32_t off;
                     if (!KMAJ) {
-                        off = (w * kRowsPerWarp / 16 + (rb >> 1)) * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
+                        // box w holds rows 16 lw.. of group gi (see the producer)
+                        off = w * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
                     } else {
-                        off = (s >> 2) * 16384 + (kRowsPerWarp * w + 8 * rb + gl) * 128 + aoff[s & 3];
+                        off = gi * (Cfg::A_BYTES / G) + (s >> 2) * (Cfg::A_BYTES / 2 / G) +
+                              (kRowsPerWarp * lw + 8 * rb + gl) * 128 + aoff[s & 3];
                     }
                     a[rb] = *reinterpret_cast<const double*>(As + off);
                 }
@@ -431,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = lane; c < C; c += 32) {
             if (!KMAJ) {
                 const long long mrows = p.L * p.I;
-                const long long mbase = tile * kBM + kRowsPerWarp * w;
+                const long long mbase = tile * p.TR + kRowsPerWarp * lw;
                 if (p.L == 1) {
                     for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
                 } else if (mbase < mrows) {
@@ -462,14 +493,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     wsb[(cur - ifirst) * C + c] = sum;
                 }
             } else if (p.flavor == kKMajorJ) {
-                const long long ti = tile % p.n_ti;
-                const long long tj = tile / p.n_ti;
+                const long long tj = div_nn(tile, p.n_ti);
+                const long long ti = tile - tj * p.n_ti;
                 if (p.BI >= kRowsPerWarp) {
                     double sc[kRowsPerWarp];
                     bool ok[kRowsPerWarp];
 #pragma unroll
                     for (int r = 0; r < kRowsPerWarp; ++r) {
-                        const int rho = kRowsPerWarp * w + r;
+                        const int rho = kRowsPerWarp * lw + r;
                         const long long i = ti * p.BI + rho % p.BI;
                         const long long j = tj * p.BJ + rho / p.BI;
                         ok[r] = i < p.I && j < p.R;
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (ok[r]) wsb[r * C + c] = Pw[r * LD + c] * sc[r];
                 } else {
                     const int njl = kRowsPerWarp / p.BI;
-                    const int jl0 = (kRowsPerWarp * w) / p.BI;
+                    const int jl0 = (kRowsPerWarp * lw) / p.BI;
                     for (int il = 0; il < p.BI; ++il) {
                         const long long i = ti * p.BI + il;
                         if (i >= p.I) continue;
@@ -493,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                const long long ibase = tile * kBM + kRowsPerWarp * w;
+                const long long ibase = tile * p.TR + kRowsPerWarp * lw;
                 for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
             }
         }

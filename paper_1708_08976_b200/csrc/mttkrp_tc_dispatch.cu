@@ -5,7 +5,7 @@ namespace dmtkg {
 
 #define DMTKG_NB(X) \
     bool launch_tc_nb##X(const TcPlan&, const CUtensorMap&, int, bool, int, cudaStream_t); \
-    int tc_smem_nb##X(int);
+    int tc_smem_nb##X(int, int, int);
 DMTKG_NB(1) DMTKG_NB(2) DMTKG_NB(3) DMTKG_NB(4) DMTKG_NB(5) DMTKG_NB(6) DMTKG_NB(7) DMTKG_NB(8)
 #undef DMTKG_NB
 
@@ -24,16 +24,16 @@ bool launch_mttkrp_tc(const TcPlan& p, const CUtensorMap& map, int nb, int tail,
     }
 }
 
-int tc_smem_bytes(int nb, int tail) {
+int tc_smem_bytes(int nb, int tail, int G, int stages) {
     switch (nb) {
-        case 1: return tc_smem_nb1(tail);
-        case 2: return tc_smem_nb2(tail);
-        case 3: return tc_smem_nb3(tail);
-        case 4: return tc_smem_nb4(tail);
-        case 5: return tc_smem_nb5(tail);
-        case 6: return tc_smem_nb6(tail);
-        case 7: return tc_smem_nb7(tail);
-        case 8: return tc_smem_nb8(tail);
+        case 1: return tc_smem_nb1(tail, G, stages);
+        case 2: return tc_smem_nb2(tail, G, stages);
+        case 3: return tc_smem_nb3(tail, G, stages);
+        case 4: return tc_smem_nb4(tail, G, stages);
+        case 5: return tc_smem_nb5(tail, G, stages);
+        case 6: return tc_smem_nb6(tail, G, stages);
+        case 7: return tc_smem_nb7(tail, G, stages);
+        case 8: return tc_smem_nb8(tail, G, stages);
         default: return -1;
     }
 }

@@ -8,9 +8,8 @@ namespace dmtkg {
 template <int TAIL, bool KM>
 static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaStream_t s) {
     auto k = mttkrp_tc_kernel<8, TAIL, KM>;
-    const int smem = TcCfg<8, TAIL>::SMEM;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<grid, kThreads, smem, s>>>(map, p);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+    k<<<grid, kThreads, p.smem, s>>>(map, p);
 }
 
 bool launch_tc_nb8(const TcPlan& p, const CUtensorMap& map, int tail, bool kmajor, int grid, cudaStream_t s) {
@@ -27,12 +26,18 @@ bool launch_tc_nb8(const TcPlan& p, const CUtensorMap& map, int tail, bool kmajo
     }
 }
 
-int tc_smem_nb8(int tail) {
+template <int TAIL>
+static int smem_of(int G, int stages) {
+    using Cfg = TcCfg<8, TAIL>;
+    return Cfg::FIXED + stages * (Cfg::A_BYTES + G * Cfg::B_BYTES);
+}
+
+int tc_smem_nb8(int tail, int G, int stages) {
     switch (tail) {
-        case 0: return TcCfg<8, 0>::SMEM;
-        case 1: return TcCfg<8, 1>::SMEM;
-        case 2: return TcCfg<8, 2>::SMEM;
-        case 4: return TcCfg<8, 4>::SMEM;
+        case 0: return smem_of<0>(G, stages);
+        case 1: return smem_of<1>(G, stages);
+        case 2: return smem_of<2>(G, stages);
+        case 4: return smem_of<4>(G, stages);
         default: return -1;
     }
 }
