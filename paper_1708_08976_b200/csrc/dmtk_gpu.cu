@@ -255,8 +255,14 @@ static bool tail_of(int C, int& nb, int& tail) {
     if (C < 1 || C > 64) return false;
     nb = C / 8;
     int t = C % 8;
+    // DFMA tail only for 1-2 leftover columns: wider tails cost more on the
+    // shared FP64 pipe (and in issue slots) than padding one more DMMA group
+    static const int max_tail = [] {
+        const char* e = std::getenv("DMTK_GPU_MAX_TAIL");
+        return e ? std::atoi(e) : 2;
+    }();
     if (t == 3) t = 4;
-    if (t > 4) {
+    if (t > max_tail) {
         ++nb;
         t = 0;
     }
@@ -288,7 +294,7 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
     for (int G : {1, 2, 4}) {
         if (G > max_g) break;
         const int TR = kBM / G;
-        const double gpen = 1.0 + 0.02 * (G - 1);
+        const double gpen = G == 1 ? 1.0 : (G == 2 ? 1.02 : 1.4);  // builder load per X byte grows with G
         if (flavor == kKMajorJ) {
             for (int bi = TR; bi >= 1; bi /= 2) {
                 const int bj = TR / bi;
@@ -349,6 +355,7 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
     int max_g = 1;  // row groups whose B tiles still leave room for a 2-stage ring
     for (int g : {2, 4})
         if (tc_smem_bytes(mp.nb, mp.tail, g, 2) <= 227 * 1024) max_g = g;
+    if (const char* fg = std::getenv("DMTK_GPU_MAX_G")) max_g = std::min(max_g, std::max(1, std::atoi(fg)));
     if (mp.kind == kTcM) {
         p.flavor = kMMajor;
         tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, max_g);

@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // shared-window addresses, computed once (no per-stage address conversion)
+    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 2);  // producer expect_tx + the stage's builder warp
@@ -118,13 +120,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int slot = cur.slot;
                 const long long tile = cur.tile;
                 const long long st = cur.st;
-                mbar_wait(&empty[slot], cur.ph ^ 1u);
+                mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
                 if (p.debug & 2) {
-                    mbar_arrive(&full[slot]);
+                    mbar_arrive_a(full_a + 8 * slot);
                     continue;
                 }
-                mbar_arrive_expect_tx(&full[slot], Cfg::A_BYTES);
-                unsigned char* dst = sA + slot * Cfg::A_BYTES;
+                mbar_arrive_expect_tx_a(full_a + 8 * slot, Cfg::A_BYTES);
+                const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
                 const int gshift = 4 - __ffs(G);  // log2(8 / G): consumer warps (and 16-row boxes) per group
                 if (!KMAJ) {
                     // 8 boxes {16 m, 32 j}: box b is row group b >> gshift,
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int j0 = static_cast<int>(st * kBK * G);
 #pragma unroll
                     for (int b = 0; b < 8; ++b)
-                        tma_load_2d(dst + b * 4096, &tmap, &full[slot], m0 + 16 * (b & ((1 << gshift) - 1)),
+                        tma_load_2d(dst + b * 4096, &tmap, full_a + 8 * slot, m0 + 16 * (b & ((1 << gshift) - 1)),
                                     j0 + kBK * (b >> gshift), pol);
                 } else {
                     long long ti, tj, j, l0;
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int gi = 0; gi < G; ++gi) {
 #pragma unroll
                             for (int h = 0; h < 2; ++h)
-                                tma_load_3d(dst + gi * gbytes + h * (gbytes / 2), &tmap, &full[slot],
+                                tma_load_3d(dst + gi * gbytes + h * (gbytes / 2), &tmap, full_a + 8 * slot,
                                             static_cast<int>(l0 + kBK * gi + 16 * h), static_cast<int>(ti * p.BI),
                                             static_cast<int>(j), pol);
                         }
@@ -189,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
                 if (mine != bw) continue;
                 if (p.debug & 1) {
-                    mbar_wait(&empty[cur.slot], cur.ph ^ 1u);
+                    mbar_wait_a(empty_a + 8 * cur.slot, cur.ph ^ 1u);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[cur.slot]);
+                    if (lane == 0) mbar_arrive_a(full_a + 8 * cur.slot);
                     continue;
                 }
                 const int slot = cur.slot;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (gi == 0 && ch == 0) mbar_wait(&empty[slot], ph ^ 1u);
+                    if (gi == 0 && ch == 0) mbar_wait_a(empty_a + 8 * slot, ph ^ 1u);
 #pragma unroll
                     for (int sp = 0; sp < SPC / 2; ++sp) {
                         const int s2 = ch * SPC / 2 + sp;
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }  // row groups
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full[slot]);
+            if (lane == 0) mbar_arrive_a(full_a + 8 * slot);
         }
         return;
     }
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
         const int slot = cur.slot;
         const long long tile = cur.tile;
-        mbar_wait(&full[slot], cur.ph);
+        mbar_wait_a(full_a + 8 * slot, cur.ph);
         const unsigned char* As = sA + slot * Cfg::A_BYTES;
         const double* Bm = reinterpret_cast<const double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
         const double* Bt = Bm + Cfg::BMAIN;
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0) mbar_arrive_a(empty_a + 8 * slot);
 
         const bool seg_end = (gs + 1 == hi) || (cur.st + 1 == spt);
         if (!seg_end) continue;
