@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int r = 0; r < kRowsPerWarp; ++r) {
                         long long l = l0 + r;
-                        if (l >= p.L) l -= p.L * div_nn(l, p.L);
+                        if (l >= p.L) l = p.L >= kRowsPerWarp ? l - p.L : l - p.L * div_nn(l, p.L);
                         sc[r] = (mbase + r < mrows) ? krp_scale(p.sgen, l, c) : 0.0;
                     }
                     long long l = l0;
