@@ -382,53 +382,97 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     double* Pw = sEpi + w * kRowsPerWarp * Cfg::EPI_LD;
     int seg = 0;
+
+    // Fragments of one k4-step pair, double-buffered in registers: the loads
+    // of the next pair (across the stage boundary too: the next stage's full
+    // barrier is awaited before this stage's last DMMAs) overlap the DMMAs
+    // of the current one, so the tensor pipe sees no stage-boundary bubble.
+    struct Frag {
+        double2 bv[NB];
+        double a[2][kRB];
+        double bt[2][TAIL > 0 ? TAIL : 1];
+    };
+    const uint32_t a_warp = KMAJ ? static_cast<uint32_t>(gi * (Cfg::A_BYTES / G) + (kRowsPerWarp * lw + gl) * 128)
+                                 : static_cast<uint32_t>(w * 4096);
+    const uint32_t a_box = KMAJ ? static_cast<uint32_t>(Cfg::A_BYTES / 2 / G) : 0u;
+    auto load = [&](Frag& f, int sl, int s2) {
+        const unsigned char* As = sA + sl * Cfg::A_BYTES;
+        const double* Bm = reinterpret_cast<const double*>(sB + sl * GB_BYTES + gi * Cfg::B_BYTES);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+            f.bv[nb] = *reinterpret_cast<const double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1));
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+            const int s = 2 * s2 + sub;
+#pragma unroll
+            for (int rb = 0; rb < kRB; ++rb) {
+                const uint32_t off = !KMAJ ? a_warp + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)]
+                                           : a_warp + (s >> 2) * a_box + 8 * rb * 128 + aoff[s & 3];
+                f.a[sub][rb] = *reinterpret_cast<const double*>(As + off);
+            }
+            if (TAIL > 0) {
+                const double* Bt = Bm + Cfg::BMAIN;
+#pragma unroll
+                for (int tc = 0; tc < TAIL; ++tc) f.bt[sub][tc] = Bt[(s * 4 + tl) * (TAIL > 0 ? TAIL : 1) + tc];
+            }
+        }
+    };
+    auto compute = [&](const Frag& f) {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+#pragma unroll
+            for (int rb = 0; rb < kRB; ++rb) {
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+                    dmma_8x8x4(acc[rb][nb][0], acc[rb][nb][1], f.a[sub][rb], sub ? f.bv[nb].y : f.bv[nb].x);
+            }
+            if (TAIL > 0) {
+#pragma unroll
+                for (int rb = 0; rb < kRB; ++rb) {
+#pragma unroll
+                    for (int tc = 0; tc < TAIL; ++tc)
+                        tacc[rb][tc] = fma(f.a[sub][rb], f.bt[sub][tc], tacc[rb][tc]);
+                }
+            }
+        }
+    };
+
+    // Cross-stage prefetch needs two fragment sets live; above 3 column
+    // groups that pushes the kernel past its register budget (spills cost
+    // more than the bubble), so wide ranks load per pair instead.
+    constexpr bool kPrefetch = NB <= 3;
     StageCursor cur;
     cur.init(lo, spt);
+    Frag f0, f1;
+    if (kPrefetch && lo < hi) {
+        mbar_wait_a(full_a + 8 * cur.slot, cur.ph);
+        load(f0, cur.slot, 0);
+    }
     for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
         const int slot = cur.slot;
         const long long tile = cur.tile;
-        mbar_wait_a(full_a + 8 * slot, cur.ph);
-        const unsigned char* As = sA + slot * Cfg::A_BYTES;
-        const double* Bm = reinterpret_cast<const double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
-        const double* Bt = Bm + Cfg::BMAIN;
+        if (kPrefetch) {
+            StageCursor nxt = cur;
+            nxt.next(spt, STAGES);
+            const bool has_next = gs + 1 < hi;
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-            double2 bv[NB];
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
-                bv[nb] = *reinterpret_cast<const double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1));
-#pragma unroll
-            for (int sub = 0; sub < 2; ++sub) {
-                const int s = 2 * s2 + sub;
-                double a[kRB];
-#pragma unroll
-                for (int rb = 0; rb < kRB; ++rb) {
-                    uint32_t off;
-                    if (!KMAJ) {
-                        // box w holds rows 16 lw.. of group gi (see the producer)
-                        off = w * 4096 + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)];
-                    } else {
-                        off = gi * (Cfg::A_BYTES / G) + (s >> 2) * (Cfg::A_BYTES / 2 / G) +
-                              (kRowsPerWarp * lw + 8 * rb + gl) * 128 + aoff[s & 3];
-                    }
-                    a[rb] = *reinterpret_cast<const double*>(As + off);
+            for (int s2 = 0; s2 < 4; ++s2) {
+                Frag& cf = (s2 & 1) ? f1 : f0;
+                Frag& nf = (s2 & 1) ? f0 : f1;
+                if (s2 < 3) {
+                    load(nf, slot, s2 + 1);
+                } else if (has_next) {
+                    mbar_wait_a(full_a + 8 * nxt.slot, nxt.ph);
+                    load(nf, nxt.slot, 0);
                 }
+                compute(cf);
+            }
+        } else {
+            mbar_wait_a(full_a + 8 * slot, cur.ph);
 #pragma unroll
-                for (int rb = 0; rb < kRB; ++rb) {
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb)
-                        dmma_8x8x4(acc[rb][nb][0], acc[rb][nb][1], a[rb], sub ? bv[nb].y : bv[nb].x);
-                }
-                if (TAIL > 0) {
-                    double bt[TAIL > 0 ? TAIL : 1];
-#pragma unroll
-                    for (int tc = 0; tc < TAIL; ++tc) bt[tc] = Bt[(s * 4 + tl) * TAIL + tc];
-#pragma unroll
-                    for (int rb = 0; rb < kRB; ++rb) {
-#pragma unroll
-                        for (int tc = 0; tc < TAIL; ++tc) tacc[rb][tc] = fma(a[rb], bt[tc], tacc[rb][tc]);
-                    }
-                }
+            for (int s2 = 0; s2 < 4; ++s2) {
+                load(f0, slot, s2);
+                compute(f0);
             }
         }
         __syncwarp();
