@@ -1155,17 +1155,19 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             *zero_tensor = 1;
             return;
         }
-        // device state: factors | lambda | M | H | normx | fit(iters x 4) | solve scratch
+        // device state: factors | lambda | M | H | Grams (N x C x C) | normx | fits | solve scratch
         DevBuf F, M, aux;
         F.ensure(static_cast<size_t>(ftot));
         M.ensure(static_cast<size_t>(maxrows * C));
         const int iters = cfg->max_iters;
-        aux.ensure(static_cast<size_t>(64 + 64 * 64 + 1 + 4 * std::max(iters, 1) + 3 * 64 * 64 + 64));
+        const int fit_slots = std::max(iters, 1) + 1;
+        aux.ensure(static_cast<size_t>(64 + 64 * 64 + N * C * C + 1 + 4 * fit_slots + 3 * 64 * 64 + 64));
         double* lam = aux.p;
         double* H = lam + 64;
-        double* dnorm = H + 64 * 64;
-        double* fitb = dnorm + 1;
-        double* solve_scr = fitb + 4 * std::max(iters, 1);
+        double* grams = H + 64 * 64;
+        double* dnorm = grams + N * C * C;
+        double* fitb = dnorm + 1;           // slot 0: the graph's fit output; 1..iters: history
+        double* solve_scr = fitb + 4 * fit_slots;
         CK(cudaMemcpyAsync(F.p, hf.data(), hf.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dnorm, &normx, sizeof(double), cudaMemcpyHostToDevice, s));
         launch_fill(lam, C, 1.0, s);
@@ -1177,42 +1179,105 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             Um[k] = F.p + off;
             Uc[k] = Um[k];
             off += t->dims[k] * C;
+            launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
+            check_launch("gram");
         }
-        std::vector<cudaEvent_t> evs(static_cast<size_t>(N + 1));
+        // one mode of als_iterate (cp_als.cpp:134-153): MTTKRP, Gram-Hadamard
+        // from the cached Grams, solve, normalise, refresh this mode's Gram
+        auto mode_step = [&](int n) {
+            mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
+            launch_hadamard_grams(grams, N, C, n, H, s);
+            check_launch("hadamard_grams");
+            launch_solve_psd(H, C, M.p, t->dims[n], Um[n], solve_scr, ctx.flag, s);
+            count_launch(4);
+            ck(cudaGetLastError(), "solve_psd");
+            launch_normalize_cols(Um[n], t->dims[n], C, lam, s);
+            check_launch("normalize");
+            launch_gram(Um[n], t->dims[n], C, grams + static_cast<long long>(n) * C * C, s);
+            check_launch("gram");
+        };
+        // H and M still hold the last mode's values (cp_als.cpp:149-155)
+        auto fit_step = [&]() {
+            launch_fit_cached(Um[N - 1], M.p, t->dims[N - 1], C, lam, H, grams + static_cast<long long>(N - 1) * C * C,
+                              dnorm, fitb, s);
+            check_launch("fit");
+        };
+        // Iteration 1 runs eagerly (it builds every plan, CSR map and buffer);
+        // the later ones replay per-mode CUDA graphs of the same launches.
+        std::vector<cudaGraphExec_t> gexec(static_cast<size_t>(N + 1), nullptr);
+        std::vector<long long> gkernels(static_cast<size_t>(N + 1), 0);
+        bool graphs = false;
+        std::vector<cudaEvent_t> evs(static_cast<size_t>(std::max(iters, 1)) * (N + 1));
         for (auto& e : evs) CK(cudaEventCreate(&e));
+        std::vector<double> f4(4 * fit_slots, 0.0);
         double prev_fit = 0.0;
         int done = 0;
         for (int iter = 1; iter <= iters; ++iter) {
-            for (int n = 0; n < N; ++n) {  // als_iterate, cp_als.cpp:134-153
-                CK(cudaEventRecord(evs[n], s));
-                mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
-                gram_hadamard_dev(ctx, t->dims, Uc, C, n, H, s);
-                launch_solve_psd(H, C, M.p, t->dims[n], Um[n], solve_scr, ctx.flag, s);
-                count_launch(4);
-                ck(cudaGetLastError(), "solve_psd");
-                launch_normalize(Um[n], t->dims[n], C, lam, s);
-                check_launch("normalize");
+            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * (N + 1);
+            for (int n = 0; n <= N; ++n) {
+                if (n < N) CK(cudaEventRecord(ev[n], s));
+                if (graphs) {
+                    CK(cudaGraphLaunch(gexec[n], s));
+                    count_launch(static_cast<int>(gkernels[n]));
+                } else {
+                    n < N ? mode_step(n) : fit_step();
+                }
+                if (n == N - 1) CK(cudaEventRecord(ev[N], s));
             }
-            CK(cudaEventRecord(evs[N], s));
-            // H, M hold the last mode's values (cp_als.cpp:149-155)
-            launch_fit(Um[N - 1], M.p, t->dims[N - 1], C, lam, H, dnorm, fitb + 4 * (iter - 1), s);
-            check_launch("fit");
-            double f4[4];
-            CK(cudaMemcpyAsync(f4, fitb + 4 * (iter - 1), sizeof(f4), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            CK(cudaMemcpyAsync(fitb + 4 * iter, fitb, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            if (iter == 1 && iters > 1) {  // capture after the eager warm-up iteration
+                bool ok = true;
+                for (int n = 0; n <= N && ok; ++n) {
+                    cudaGraph_t g = nullptr;
+                    const long long before = g_launches.load();
+                    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                        ok = false;
+                        break;
+                    }
+                    try {
+                        n < N ? mode_step(n) : fit_step();
+                    } catch (const Err&) {
+                        ok = false;
+                    }
+                    const cudaError_t ec = cudaStreamEndCapture(s, &g);
+                    if (!ok || ec != cudaSuccess || !g || cudaGraphInstantiate(&gexec[n], g, 0) != cudaSuccess) ok = false;
+                    if (g) cudaGraphDestroy(g);
+                    gkernels[n] = g_launches.load() - before;
+                    g_launches.fetch_sub(gkernels[n]);  // captured, not launched
+                }
+                cudaGetLastError();
+                graphs = ok;
+                if (!ok)
+                    for (auto& ge : gexec)
+                        if (ge) {
+                            cudaGraphExecDestroy(ge);
+                            ge = nullptr;
+                        }
+            }
+            done = iter;
+            if (cfg->tol > 0.0) {  // the stopping rule needs this iteration's fit on the host
+                CK(cudaMemcpyAsync(f4.data() + 4 * iter, fitb + 4 * iter, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                if (iter > 1 && std::fabs(f4[4 * iter] - prev_fit) < cfg->tol) break;
+                prev_fit = f4[4 * iter];
+            }
+        }
+        CK(cudaMemcpyAsync(f4.data(), fitb, 4 * fit_slots * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int iter = 1; iter <= done; ++iter) {
+            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * (N + 1);
             float ms_total = 0;
             for (int n = 0; n < N; ++n) {
                 float ms;
-                CK(cudaEventElapsedTime(&ms, evs[n], evs[n + 1]));
+                CK(cudaEventElapsedTime(&ms, ev[n], n + 1 < N ? ev[n + 1] : ev[N]));
                 if (mode_seconds_out) mode_seconds_out[(iter - 1) * N + n] = ms * 1e-3;
                 ms_total += ms;
             }
             if (iter_seconds_out) iter_seconds_out[iter - 1] = ms_total * 1e-3;
-            fits_out[iter - 1] = f4[0];
-            done = iter;
-            if (iter > 1 && std::fabs(f4[0] - prev_fit) < cfg->tol) break;
-            prev_fit = f4[0];
+            fits_out[iter - 1] = f4[4 * iter];
         }
+        for (auto& ge : gexec)
+            if (ge) cudaGraphExecDestroy(ge);
         for (auto& e : evs) cudaEventDestroy(e);
         CK(cudaMemcpyAsync(factors_out, F.p, static_cast<size_t>(ftot) * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (done > 0) {

@@ -382,6 +382,105 @@ __global__ void sumsq_final_kernel(const double* __restrict__ part, int n, doubl
     }
 }
 
+// ------------------------------------------------- CP-ALS, cached Grams
+// G = U^T U, one warp per upper-triangle entry: lane-strided row partial sums
+// then a fixed xor-tree, mirrored to the lower triangle (symmetric to the bit,
+// like linalg.cpp:210-226; deterministic run to run).
+__global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ G) {
+    int e = blockIdx.x, c1 = 0;
+    while (e >= C - c1) {  // blockIdx -> (c1, c2 >= c1)
+        e -= C - c1;
+        ++c1;
+    }
+    const int c2 = c1 + e;
+    double s = 0.0;
+    for (long long r = threadIdx.x; r < rows; r += 32) s = fma(U[r * C + c1], U[r * C + c2], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+        G[c1 * C + c2] = s;
+        G[c2 * C + c1] = s;
+    }
+}
+
+// H = Hadamard of the cached Grams of every mode but `skip` (linalg.cpp:228-248).
+__global__ void hadamard_grams_kernel(const double* __restrict__ grams, int nmodes, int C, int skip,
+                                      double* __restrict__ H) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= C * C) return;
+    double h = 1.0;
+    for (int k = 0; k < nmodes; ++k)
+        if (k != skip) h *= grams[static_cast<long long>(k) * C * C + e];
+    H[e] = h;
+}
+
+// Column 2-norms into lambda and column scaling (cp_als.cpp:101-118); one
+// CTA per column, fixed-order tree reduction.
+__global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda) {
+    __shared__ double red[256];
+    __shared__ double s_norm;
+    const int c = blockIdx.x;
+    double sq = 0.0;
+    for (long long r = threadIdx.x; r < rows; r += blockDim.x) {
+        const double v = U[r * C + c];
+        sq = fma(v, v, sq);
+    }
+    red[threadIdx.x] = sq;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s_norm = sqrt(red[0]);
+        lambda[c] = s_norm;
+    }
+    __syncthreads();
+    const double nrm = s_norm;
+    if (nrm > 0.0) {
+        const double inv = 1.0 / nrm;
+        for (long long r = threadIdx.x; r < rows; r += blockDim.x) U[r * C + c] *= inv;
+    }
+}
+
+// Fit from the last mode with the cached Gram of the (updated) last factor
+// (cp_als.cpp:34-72).
+__global__ void fit_cached_kernel(const double* __restrict__ U, const double* __restrict__ Mlast, long long rows, int C,
+                                  const double* __restrict__ lambda, const double* __restrict__ Hlast,
+                                  const double* __restrict__ Glast, const double* __restrict__ normx,
+                                  double* __restrict__ out) {
+    __shared__ double red[256];
+    double inner = 0.0;
+    for (long long e = threadIdx.x; e < rows * C; e += blockDim.x) {
+        const int c = static_cast<int>(e % C);
+        inner += Mlast[e] * lambda[c] * U[e];
+    }
+    red[threadIdx.x] = inner;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double in = red[0];
+        double ny = 0.0;
+        for (int c1 = 0; c1 < C; ++c1)
+            for (int c2 = 0; c2 < C; ++c2) ny += lambda[c1] * lambda[c2] * Hlast[c1 * C + c2] * Glast[c1 * C + c2];
+        const double nx = normx[0];
+        double res2 = nx * nx - 2.0 * in + ny;
+        if (res2 < 0.0) res2 = 0.0;
+        const double ar = sqrt(res2);
+        out[2] = ar;
+        if (nx > 0.0) {
+            out[1] = ar / nx;
+            out[0] = 1.0 - out[1];
+            out[3] = 1.0;
+        } else {
+            out[0] = out[1] = out[3] = 0.0;
+        }
+    }
+}
+
 // --------------------------------------------------------- FP64 peak probe
 __global__ void dmma_peak_kernel(double* out, int iters) {
     double acc[8][2];
@@ -460,6 +559,23 @@ void launch_fit(const double* U, const double* Mlast, long long rows, int C, con
 void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s) {
     sumsq_partial_kernel<<<nparts, 512, 0, s>>>(x, n, part);
     sumsq_final_kernel<<<1, 32, 0, s>>>(part, nparts, out);
+}
+
+void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s) {
+    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, G);
+}
+
+void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s) {
+    hadamard_grams_kernel<<<(C * C + 127) / 128, 128, 0, s>>>(grams, nmodes, C, skip, H);
+}
+
+void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
+    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda);
+}
+
+void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
+                       const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s) {
+    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, Glast, normx, out);
 }
 
 void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s) {

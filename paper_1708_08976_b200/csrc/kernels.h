@@ -24,6 +24,12 @@ void launch_fit(const double* U, const double* Mlast, long long rows, int C, con
                 const double* normx, double* out, cudaStream_t s);
 void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s);
 void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
+// CP-ALS with cached Grams
+void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
+void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
+void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s);
+void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
+                       const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s);
 
 // Tensor-core streaming MTTKRP (mttkrp_tc.cuh). nb in [1, 8], tail in
 // {0, 1, 2, 4}; returns false when no instantiation matches.

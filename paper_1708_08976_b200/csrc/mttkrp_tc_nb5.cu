@@ -8,7 +8,11 @@ namespace dmtkg {
 template <int TAIL, bool KM>
 static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaStream_t s) {
     auto k = mttkrp_tc_kernel<5, TAIL, KM>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+    static int opted = 0;  // raise the opt-in once (not a stream op: stays out of graph captures)
+    if (p.smem > opted) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        opted = 227 * 1024;
+    }
     k<<<grid, kThreads, p.smem, s>>>(map, p);
 }
 
