@@ -146,6 +146,9 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
  * roofline denominator the benchmark reports (MEASURED_PEAKS.json has no
  * FP64 entry). */
 int dmtk_gpu_fp64_peak(int device, double* tflops);
+/* The same probe run back to back for `seconds`: the settled (power-capped)
+ * rate, the denominator for kernels timed inside a long step. */
+int dmtk_gpu_fp64_peak_sustained(int device, double seconds, double* tflops);
 
 /* Number of kernels this library has launched since load (for the
  * benchmark's gpu_launches claim). */

@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     device_count,
     fit,
     fp64_peak_tflops,
+    fp64_peak_tflops_sustained,
     gram_hadamard,
     krp,
     krp_naive,

@@ -63,6 +63,7 @@ _SIGS = {
                                   C.POINTER(C.c_int), dp]),
     "dmtk_gpu_fit": (C.c_int, [T, C.c_int, dpp, i64p, i64p, dp, C.c_int64, C.c_int, dp]),
     "dmtk_gpu_fp64_peak": (C.c_int, [C.c_int, dp]),
+    "dmtk_gpu_fp64_peak_sustained": (C.c_int, [C.c_int, C.c_double, dp]),
     "dmtk_gpu_launch_count": (C.c_int64, []),
 }
 

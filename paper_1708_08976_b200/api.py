@@ -399,5 +399,11 @@ def fp64_peak_tflops(device: int = 0) -> float:
     return float(out[0])
 
 
+def fp64_peak_tflops_sustained(seconds: float = 1.0, device: int = 0) -> float:
+    out = np.zeros(1)
+    _check(lib.dmtk_gpu_fp64_peak_sustained(device, seconds, _dp(out)))
+    return float(out[0])
+
+
 def launch_count() -> int:
     return int(lib.dmtk_gpu_launch_count())

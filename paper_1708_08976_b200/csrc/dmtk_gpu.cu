@@ -153,6 +153,14 @@ static Context& context(int device) {
     if (prop.major != 10) fail(DMTK_GPU_ERUNTIME, std::string("dmtk_gpu: built for sm_100a, found ") + prop.name);
     c->sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {  // keep freed tensor memory in the device pool (see dmtk_gpu_tensor_upload)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~0ULL;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     c->ones.ensure(4096);
     launch_fill(c->ones.p, 4096, 1.0, c->stream);
@@ -867,7 +875,9 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
         t->dims = d;
         t->total = prod(d, 0, ndim);
         double* p = nullptr;
-        CK(cudaMalloc(&p, static_cast<size_t>(t->total) * sizeof(double)));
+        // stream-ordered pool allocation: repeated upload/free cycles reuse the
+        // pool instead of paying cudaMalloc/cudaFree for every 8 GB tensor
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(t->total) * sizeof(double), ctx.stream));
         t->d = p;
         t->owned = true;
         CK(cudaMemcpyAsync(p, host, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
@@ -895,8 +905,10 @@ int dmtk_gpu_tensor_free(dmtk_gpu_tensor t) {
     return guarded([&] {
         if (!t) return;
         if (t->owned && t->d) {
+            Context& ctx = context(t->device);
             cudaSetDevice(t->device);
-            cudaFree(const_cast<double*>(t->d));
+            cudaFreeAsync(const_cast<double*>(t->d), ctx.stream);
+            cudaStreamSynchronize(ctx.stream);
         }
         delete t;
     });
@@ -1325,6 +1337,38 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
         check_launch("fit");
         CK(cudaMemcpyAsync(out4, o4, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
         CK(cudaStreamSynchronize(ctx.stream));
+    });
+}
+
+int dmtk_gpu_fp64_peak_sustained(int device, double seconds, double* tflops) {
+    return guarded([&] {
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        ctx.als_small.ensure(64);
+        const int blocks = ctx.sms * 2, iters = 100000;  // ~25 ms per launch at full clock
+        const double flops = 2.0 * 256 * 8 * static_cast<double>(iters) * blocks * (256 / 32);
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        const double t_end = now_s() + seconds;
+        double best = 0.0, last = 0.0;
+        int n = 0;
+        while (now_s() < t_end || n < 2) {  // back to back, like the bf16 "sustained" peak
+            CK(cudaEventRecord(a, ctx.stream));
+            launch_dmma_peak(ctx.als_small.p, blocks, iters, ctx.stream);
+            count_launch();
+            CK(cudaEventRecord(b, ctx.stream));
+            CK(cudaEventSynchronize(b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            last = flops / (ms * 1e-3) / 1e12;
+            best = std::max(best, last);
+            ++n;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *tflops = last;  // the settled rate after `seconds` of continuous DMMA load
     });
 }
 
