@@ -299,8 +299,13 @@ static double kwaste(long long K, int G) {
 static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int max_g) {
     Tiling best{1, 128, 1};
     double best_cost = 1e300;
+    static const int force_g = [] {
+        const char* e = std::getenv("DMTK_GPU_FORCE_G");
+        return e ? std::atoi(e) : 0;
+    }();
     for (int G : {1, 2, 4}) {
         if (G > max_g) break;
+        if (force_g && G != force_g) continue;
         const int TR = kBM / G;
         const double gpen = G == 1 ? 1.0 : (G == 2 ? 1.02 : 1.4);  // builder load per X byte grows with G
         if (flavor == kKMajorJ) {
@@ -668,6 +673,19 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         mp.tc.bgen = bgen;
         mp.tc.sgen = sgen;
         mp.tc.ws = ctx.ws.p;
+        // small fastest factor: stage it in shared memory (builders read LDS)
+        // with a row pitch = 2 (mod 4) doubles (conflict-free fragment rows)
+        mp.tc.u0_pitch = 0;
+        {
+            const int P = C + ((6 - C % 4) % 4);
+            const long long bytes = bgen.ext[0] * P * 8;
+            const int padded = static_cast<int>((bytes + 127) / 128 * 128);
+            if (bgen.ext[0] >= kBK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
+                !std::getenv("DMTK_GPU_NO_U0_SMEM")) {
+                mp.tc.u0_pitch = P;
+                mp.tc.smem += padded;
+            }
+        }
         // heads = KRP of every B factor but the fastest (the reuse partial of
         // krp.cpp:53-88), materialised once so a builder's head is one row load
         mp.tc.htab = nullptr;

@@ -62,6 +62,7 @@ struct TcPlan {
     const double* htab;       // partial KRP of bgen factors 1..nf-1 (hrows x C), or null
     long long hrows;
     int smem;                 // dynamic shared memory bytes
+    int u0_pitch;             // > 0: fastest B factor staged in shared memory with this row pitch
 };
 
 // Stage range of CTA b under the stream-K split.

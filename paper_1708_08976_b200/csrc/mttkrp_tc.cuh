@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     double* sEpi = reinterpret_cast<double*>(sB + STAGES * GB_BYTES);
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sEpi) + Cfg::EPI_BYTES);
     uint64_t* empty = full + Cfg::MAX_STAGES;
+    double* sU0 = reinterpret_cast<double*>(empty + Cfg::MAX_STAGES);  // optional U0 copy (u0_pitch > 0)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 2);  // producer expect_tx + the stage's builder warp
+            mbar_init(&full[s], 1 + p.G);  // producer expect_tx + one builder item per row group
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_barrier_init();
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ producer
     if (warp == kProducerWarp) {
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol = (p.debug & 16) ? l2_evict_normal_policy() : l2_evict_first_policy();
             StageCursor cur;
             cur.init(lo, spt);
             for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
@@ -163,69 +164,134 @@ __global__ void __launch_bounds__(kThreads, 1)
             return;
         }
 
-        // ------------------------------------------------------------ builders
-        // Builder warp bw owns the stages it % kBuilderWarps == bw. Lane (g, t)
-        // produces exactly the B values DMMA lane (g, t) consumes: rows
-        // kperm(s, t) for the 8 k4-steps, columns nb*8 + g. All factor loads of a
-        // stage are issued before any is used (one L2 round trip per stage), and
-        // the stores are 128-bit, lane-contiguous (conflict-free).
-        if (warp < kFirstConsumerWarp) {
-            const int bw = warp - kFirstBuilderWarp;
-            const int g = lane >> 2;
-            const int t = lane & 3;
-            const KrpGen& Gen = p.bgen;
-            const long long e0 = Gen.ext[0];
-            const bool fast = e0 >= kBK;
-            const int C = p.C;
-            const double* __restrict__ U0 = Gen.U[0];
-            const long long ldu = Gen.ldu;
-            const long long kext = p.kext;
-            // head partial products (all factors but the fastest, times KR(j)
-            // for the one-step flavor) change only every e0 rows: cached here
-            double hv[2][NB];
-            double ht[2];
-            long long hq = -1, hj = -2;
-            StageCursor cur;
-            cur.init(lo, spt);
-            int mine = 0;
-            for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES), mine = (mine + 1 == kBuilderWarps ? 0 : mine + 1)) {
-                if (mine != bw) continue;
+    // ------------------------------------------------------------ builders
+    // Work items are (stage, row group) pairs dealt round-robin to the
+    // builder warps; every item arrives once on its stage's full barrier
+    // (count 1 + G). Lane (g, t) produces exactly the B values DMMA lane
+    // (g, t) consumes: rows kperm(s, t) for the 8 k4-steps, columns nb*8 + g,
+    // stored 128-bit and lane-contiguous (conflict-free). The fastest factor
+    // is read from a shared-memory copy when it is small (LDS latency instead
+    // of an L2 round trip per item), the head partial from the materialised
+    // head table (one row, refreshed only when the slower digits carry).
+    if (warp < kFirstConsumerWarp) {
+        const int bw = warp - kFirstBuilderWarp;
+        const int g = lane >> 2;
+        const int t = lane & 3;
+        const KrpGen& Gen = p.bgen;
+        const long long e0 = Gen.ext[0];
+        const bool fast = e0 >= kBK;
+        const int C = p.C;
+        const long long kext = p.kext;
+        const double* __restrict__ U0 = Gen.U[0];
+        const long long ldu = Gen.ldu;
+        const int P = p.u0_pitch;  // > 0: U0 staged in shared memory with this row pitch
+        if (P > 0) {
+            const int n = static_cast<int>(e0) * C;
+            for (int e = threadIdx.x - kFirstBuilderWarp * 32; e < n; e += kBuilderWarps * 32) {
+                const int r = e / C;
+                sU0[r * P + (e - r * C)] = U0[static_cast<long long>(r) * ldu + (e - r * C)];
+            }
+            named_bar_sync(1, kBuilderWarps * 32);
+        }
+        const uint32_t sU0a = smem_u32(sU0);
+        double hv[2][NB];
+        double ht[2];
+        long long hq = -1, hj = -2;
+        StageCursor cur;
+        cur.init(lo, spt);
+        int owner = 0;  // builder warp owning the next item
+        for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
+            for (int gi = 0; gi < G; ++gi, owner = (owner + 1 == kBuilderWarps ? 0 : owner + 1)) {
+                if (owner != bw) continue;
+                const int slot = cur.slot;
                 if (p.debug & 1) {
-                    mbar_wait_a(empty_a + 8 * cur.slot, cur.ph ^ 1u);
+                    mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_a(full_a + 8 * cur.slot);
+                    if (lane == 0) mbar_arrive_a(full_a + 8 * slot);
                     continue;
                 }
-                const int slot = cur.slot;
-                const uint32_t ph = cur.ph;
-                const long long st = cur.st;
-                long long kstage, jx = -1;
+                long long kbase, jx = -1;
                 if (KMAJ && p.flavor == kKMajorJK) {
-                    jx = div_nn(st, p.n_lc);
-                    kstage = (st - jx * p.n_lc) * kBK * G;
+                    jx = div_nn(cur.st, p.n_lc);
+                    kbase = (cur.st - jx * p.n_lc) * kBK * G + kBK * gi;
                 } else {
-                    kstage = st * kBK * G;
+                    kbase = cur.st * kBK * G + kBK * gi;
                 }
-                for (int gi = 0; gi < G; ++gi) {
-                const long long kbase = kstage + kBK * gi;
-                // Loads of a chunk of k4-steps are all issued before use; for wide
-                // ranks the stage is built in two chunks to bound registers.
-                constexpr int NCH = NB > 4 ? 2 : 1;
-                constexpr int SPC = 8 / NCH;
                 long long q0 = 0;
                 int r0 = 0;
                 if (fast) {
                     q0 = div_nn(kbase, e0);
                     r0 = static_cast<int>(kbase - q0 * e0);
+                    if (q0 != hq || jx != hj) {  // refresh the two head rows (q0, q0 + 1)
+                        hq = q0;
+                        hj = jx;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
+                            ht[h] = 1.0;
+                            if (p.htab) {
+                                if (q0 + h < p.hrows) {
+                                    const double* row = p.htab + (q0 + h) * C;
+#pragma unroll
+                                    for (int nb = 0; nb < NB; ++nb)
+                                        hv[h][nb] = nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
+                                    if (TAIL > 0) ht[h] = (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                }
+                            } else {
+                                const long long idx = (q0 + h) * e0;
+                                for (int f = 1; f < Gen.nf; ++f) {
+                                    const double* row = Gen.U[f] + krp_digit(Gen, f, idx) * Gen.ldu;
+#pragma unroll
+                                    for (int nb = 0; nb < NB; ++nb)
+                                        hv[h][nb] *= nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
+                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                }
+                            }
+                            if (jx >= 0) {
+                                const KrpGen& S = p.sgen;
+                                for (int f = 0; f < S.nf; ++f) {
+                                    const double* row = S.U[f] + krp_digit(S, f, jx) * S.ldu;
+#pragma unroll
+                                    for (int nb = 0; nb < NB; ++nb)
+                                        hv[h][nb] *= nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
+                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                }
+                            }
+                        }
+                    }
+                } else {
+                    hq = -1;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
+                    ht[0] = ht[1] = 1.0;
                 }
                 double* Bm = reinterpret_cast<double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
                 double* Bt = Bm + Cfg::BMAIN;
+                // wide ranks build the item in two chunks of k4-steps (registers)
+                constexpr int NCH = NB > 4 ? 2 : 1;
+                constexpr int SPC = 8 / NCH;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     double u[SPC][NB];
                     double ut[SPC];
                     bool hsel[SPC];
-                    if (fast) {
+                    if (fast && P > 0) {
+#pragma unroll
+                        for (int ss = 0; ss < SPC; ++ss) {
+                            const int kr = kperm<KMAJ>(ch * SPC + ss, t);
+                            int r = r0 + kr;
+                            hsel[ss] = r >= e0;
+                            if (hsel[ss]) r -= static_cast<int>(e0);
+                            const bool valid = kbase + kr < kext;
+                            const uint32_t srow = sU0a + static_cast<uint32_t>(r * P) * 8u;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb)
+                                u[ss][nb] = (valid && nb * 8 + g < C) ? lds_f64(srow + (nb * 8 + g) * 8) : 0.0;
+                            ut[ss] = (TAIL > 0 && valid && g < TAIL && 8 * NB + g < C) ? lds_f64(srow + (8 * NB + g) * 8)
+                                                                                   : 0.0;
+                        }
+                    } else if (fast) {
 #pragma unroll
                         for (int ss = 0; ss < SPC; ++ss) {
                             const int kr = kperm<KMAJ>(ch * SPC + ss, t);
@@ -235,67 +301,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const bool valid = kbase + kr < kext;
                             const double* row = U0 + r * ldu;
 #pragma unroll
-                            for (int nb = 0; nb < NB; ++nb) {
-                                const int c = nb * 8 + g;
-                                u[ss][nb] = (valid && c < C) ? __ldg(row + c) : 0.0;
-                            }
-                            ut[ss] = 0.0;
-                            if (TAIL > 0) {
-                                const int c = 8 * NB + g;
-                                ut[ss] = (valid && g < TAIL && c < C) ? __ldg(row + c) : 0.0;
-                            }
-                        }
-                        if (ch == 0 && (q0 != hq || jx != hj)) {
-                            hq = q0;
-                            hj = jx;
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const long long idx = (q0 + h) * e0;
-#pragma unroll
-                                for (int nb = 0; nb < NB; ++nb) hv[h][nb] = 1.0;
-                                ht[h] = 1.0;
-                                if (p.htab) {
-                                    // materialised partial KRP of the slower factors: one row
-                                    if (q0 + h < p.hrows) {
-                                        const double* row = p.htab + (q0 + h) * C;
-#pragma unroll
-                                        for (int nb = 0; nb < NB; ++nb) {
-                                            const int c = nb * 8 + g;
-                                            hv[h][nb] = c < C ? __ldg(row + c) : 0.0;
-                                        }
-                                        if (TAIL > 0) ht[h] = (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                                    }
-                                } else {
-                                    for (int f = 1; f < Gen.nf; ++f) {
-                                        const double* row = Gen.U[f] + krp_digit(Gen, f, idx) * Gen.ldu;
-#pragma unroll
-                                        for (int nb = 0; nb < NB; ++nb) {
-                                            const int c = nb * 8 + g;
-                                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                                        }
-                                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                                    }
-                                }
-                                if (jx >= 0) {
-                                    const KrpGen& S = p.sgen;
-                                    for (int f = 0; f < S.nf; ++f) {
-                                        const double* row = S.U[f] + krp_digit(S, f, jx) * S.ldu;
-#pragma unroll
-                                        for (int nb = 0; nb < NB; ++nb) {
-                                            const int c = nb * 8 + g;
-                                            hv[h][nb] *= c < C ? __ldg(row + c) : 0.0;
-                                        }
-                                        if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
-                                    }
-                                }
-                            }
+                            for (int nb = 0; nb < NB; ++nb)
+                                u[ss][nb] = (valid && nb * 8 + g < C) ? __ldg(row + nb * 8 + g) : 0.0;
+                            ut[ss] = (TAIL > 0 && valid && g < TAIL && 8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
                         }
                     } else {
                         // small fastest radix (< 32 rows): full product per entry
-                        hq = -1;
-#pragma unroll
-                        for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
-                        ht[0] = ht[1] = 1.0;
 #pragma unroll
                         for (int ss = 0; ss < SPC; ++ss) {
                             const int kr = kperm<KMAJ>(ch * SPC + ss, t);
@@ -322,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (gi == 0 && ch == 0) mbar_wait_a(empty_a + 8 * slot, ph ^ 1u);
+                    if (ch == 0) mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
 #pragma unroll
                     for (int sp = 0; sp < SPC / 2; ++sp) {
                         const int s2 = ch * SPC / 2 + sp;
@@ -337,12 +348,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (TAIL > 0 && g < TAIL) {
 #pragma unroll
                         for (int ss = 0; ss < SPC; ++ss)
-                            Bt[((ch * SPC + ss) * 4 + t) * TAIL + g] = ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
+                            Bt[((ch * SPC + ss) * 4 + t) * (TAIL > 0 ? TAIL : 1) + g] =
+                                ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
                     }
                 }
-            }  // row groups
-            __syncwarp();
-            if (lane == 0) mbar_arrive_a(full_a + 8 * slot);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(full_a + 8 * slot);
+            }
         }
         return;
     }
@@ -480,6 +492,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         const bool seg_end = (gs + 1 == hi) || (cur.st + 1 == spt);
         if (!seg_end) continue;
+        if (p.debug & 8) {  // experiment: drop the epilogue entirely
+#pragma unroll
+            for (int rb = 0; rb < kRB; ++rb)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
+            ++seg;
+            continue;
+        }
 
         // ------------------------------------------------- epilogue (warp-local)
         constexpr int LD = Cfg::EPI_LD;
@@ -511,8 +531,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const long long mbase = tile * p.TR + kRowsPerWarp * lw;
                 if (p.L == 1) {
                     for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
+                } else if (mbase + kRowsPerWarp <= mrows && p.L >= kRowsPerWarp && p.sgen.nf == 1) {
+                    // common multi-TTV case: 16 full rows, l wraps at most once,
+                    // a single (materialised or one-input) scale factor
+                    const long long ifirst = div_nn(mbase, p.L);
+                    const int l0 = static_cast<int>(mbase - ifirst * p.L);
+                    const int rw = static_cast<int>(p.L) - l0;  // first row of the next i
+                    const double* sbase = p.sgen.U[0] + c;
+                    const long long ldu = p.sgen.ldu;
+                    double sc[kRowsPerWarp];
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r) {
+                        const int l = r < rw ? l0 + r : l0 + r - static_cast<int>(p.L);
+                        sc[r] = __ldg(sbase + l * ldu);
+                    }
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int r = 0; r < kRowsPerWarp; ++r) {
+                        const double v = Pw[r * LD + c] * sc[r];
+                        if (r < rw) s0 += v; else s1 += v;
+                    }
+                    wsb[c] = s0;
+                    if (rw < kRowsPerWarp) wsb[C + c] = s1;
                 } else if (mbase < mrows) {
-                    // scale rows by KL(l, c): all loads issued before use
+                    // general case: partial rows, short L, multi-factor scales
                     const long long ifirst = div_nn(mbase, p.L);
                     const long long l0 = mbase - ifirst * p.L;
                     double sc[kRowsPerWarp];
