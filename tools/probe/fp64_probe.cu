@@ -91,6 +91,36 @@ __global__ void fill_kernel(double* x, size_t n) {
     x[i] = (double)(i & 1023) * 1e-3;
 }
 
+// warps [0, dmma_warps) issue DMMA, the rest DFMA: does the FP64 vector pipe
+// run concurrently with the FP64 tensor pipe?
+__global__ void mixed_kernel(double* out, int iters, int dmma_warps, double a0, double b0) {
+  const int w = threadIdx.x >> 5;
+  double s = 0;
+  if (w < dmma_warps) {
+    double acc[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { acc[k][0] = 0; acc[k][1] = 0; }
+    double a = 1.0 + threadIdx.x * 1e-6, b = 0.5;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dmma884(acc[k], a, b);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += acc[k][0] + acc[k][1];
+  } else {
+    double r[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) r[k] = threadIdx.x * 1e-3 + k;
+    for (int it = 0; it < iters * 8; ++it) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) r[k] = fma(r[k], a0, b0);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += r[k];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
@@ -143,6 +173,21 @@ int main() {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     double flops = 2.0 * 16 * 8 * 16 * 4 * iters * (double)grid * (tpb / 32);
     std::printf("DMMA16816 tpb %d: %.2f TFLOP/s (%.3f ms)\n", tpb, flops / ms / 1e9, ms);
+  }
+  {
+    // per warp per iter: DMMA warp 8*512 flop, DFMA warp 8*16*32*2 = 8192 flop
+    const int tpb = 512, grid = sms;
+    for (int dw : {16, 8, 12, 4, 0}) {
+      int iters = 2000;
+      mixed_kernel<<<grid, tpb>>>(out, 10, dw, 1.0000001, 1e-9);
+      CK(cudaEventRecord(e0));
+      mixed_kernel<<<grid, tpb>>>(out, iters, dw, 1.0000001, 1e-9);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      double fl = (double)grid * iters * (dw * 8.0 * 512 + (16 - dw) * 8.0 * 16 * 32 * 2);
+      std::printf("MIXED dmma_warps %d/16: %.2f TFLOP/s (%.3f ms)\n", dw, fl / ms / 1e9, ms);
+    }
   }
   size_t n = (size_t)1 << 30;  // 8 GiB of doubles
   double* x;
