@@ -282,49 +282,71 @@ static bool tail_of(int C, int& nb, int& tail) {
     return nb <= 8;
 }
 
-// Row-group count G (tile rows TR = 128 / G, each stage contracting 32 * G
-// indices split over the groups) and K-major row tile BI x BJ = TR, chosen to
-// minimise padded work: tile rows beyond the extent and contraction indices
-// beyond K are both zero-filled DMMA work. Smaller G wins near-ties (fewer B
-// rows to build per byte of X).
+// Tile shape: RB (rows per consumer warp 8 RB, tile BM = 64 RB rows, BK =
+// tc_bk(RB) contraction indices per stage and row group), row-group count G
+// (TR = BM / G rows, each group contracting its own BK-index slice of a
+// stage) and, K-major, the row tile BI x BJ = TR. Chosen to minimise the
+// modelled cost: zero-filled DMMA work (tile rows beyond the extent,
+// contraction indices beyond K) x builder pressure.
+// The builders are bound by their item rate (an item = one row group's B
+// tile of one stage; each waits on a factor-row load), so the pressure is
+// items per byte of X: b = G * 32 KB / A_BYTES (1 for RB 2 or 4 at G = 1,
+// 4/3 for RB 3). Measured on 1000^3 / 180^4 / fMRI shapes (r01 sweep):
+// b = 4/3 costs ~5%, b = 2 ~20%, b = 4 ~55%; RB 2 wins near-ties by ~1%.
 struct Tiling {
-    int G, BI, BJ;
+    int RB, G, BI, BJ;
 };
 
-static double kwaste(long long K, int G) {
-    const long long step = 32LL * G;
+static double kwaste(long long K, long long step) {
     return static_cast<double>(((K + step - 1) / step) * step) / static_cast<double>(K);
 }
 
-static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int max_g) {
-    Tiling best{1, 128, 1};
+static double tile_cost(int RB, int G) {
+    const double a_kb = tc_bm(RB) * tc_bk(RB) * 8 / 1024.0;
+    const double b = G * 32.0 / a_kb - 1.0;
+    return (1.0 + 0.15 * b + 0.08 * b * b) * (RB == 2 ? 1.0 : 1.01);
+}
+
+static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int nb, int tail,
+                             int max_g_rb2) {
+    Tiling best{2, 1, 128, 1};
     double best_cost = 1e300;
     static const int force_g = [] {
         const char* e = std::getenv("DMTK_GPU_FORCE_G");
         return e ? std::atoi(e) : 0;
     }();
-    for (int G : {1, 2, 4}) {
-        if (G > max_g) break;
-        if (force_g && G != force_g) continue;
-        const int TR = kBM / G;
-        const double gpen = G == 1 ? 1.0 : (G == 2 ? 1.02 : 1.4);  // builder load per X byte grows with G
-        if (flavor == kKMajorJ) {
-            for (int bi = TR; bi >= 1; bi /= 2) {
-                const int bj = TR / bi;
-                const double area = static_cast<double>(((rows_or_I + bi - 1) / bi) * bi) *
-                                    static_cast<double>(((R + bj - 1) / bj) * bj);
-                const double cost = area / (static_cast<double>(rows_or_I) * R) * kwaste(K, G) * gpen;
+    static const int force_rb = [] {
+        const char* e = std::getenv("DMTK_GPU_FORCE_RB");
+        return e ? std::atoi(e) : 0;
+    }();
+    for (int RB : {4, 3, 2}) {
+        if (!tc_has_tile(nb, tail, RB) || (force_rb && RB != force_rb)) continue;
+        for (int G : {1, 2, 4}) {
+            if (RB == 2 && G > max_g_rb2) break;
+            if (force_g && G != force_g) continue;
+            const int TR = tc_bm(RB) / G;
+            const long long step = static_cast<long long>(tc_bk(RB)) * G;
+            const double shape = tile_cost(RB, G);
+            if (flavor == kKMajorJ) {
+                for (int bi = TR; bi >= 1; bi /= 2) {
+                    if (TR % bi) continue;
+                    const int bj = TR / bi;
+                    const double area = static_cast<double>(((rows_or_I + bi - 1) / bi) * bi) *
+                                        static_cast<double>(((R + bj - 1) / bj) * bj);
+                    const double cost = area / (static_cast<double>(rows_or_I) * R) * kwaste(K, step) * shape;
+                    if (cost < best_cost - 1e-9) {
+                        best_cost = cost;
+                        best = {RB, G, bi, bj};
+                    }
+                }
+            } else {
+                const double pad =
+                    static_cast<double>(((rows_or_I + TR - 1) / TR) * TR) / static_cast<double>(rows_or_I);
+                const double cost = pad * kwaste(K, step) * shape;
                 if (cost < best_cost - 1e-9) {
                     best_cost = cost;
-                    best = {G, bi, bj};
+                    best = {RB, G, TR, 1};
                 }
-            }
-        } else {
-            const double pad = static_cast<double>(((rows_or_I + TR - 1) / TR) * TR) / static_cast<double>(rows_or_I);
-            const double cost = pad * kwaste(K, G) * gpen;
-            if (cost < best_cost - 1e-9) {
-                best_cost = cost;
-                best = {G, TR, 1};
             }
         }
     }
@@ -365,49 +387,56 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
     p.I = mp.I;
     p.R = mp.R;
     Tiling tl;
-    int max_g = 1;  // row groups whose B tiles still leave room for a 2-stage ring
+    int max_g = 1;  // 128-row tiles: row groups whose B tiles still leave room for a 2-stage ring
     for (int g : {2, 4})
-        if (tc_smem_bytes(mp.nb, mp.tail, g, 2) <= 227 * 1024) max_g = g;
+        if (tc_smem_bytes(mp.nb, mp.tail, g, 2, 2) <= 227 * 1024) max_g = g;
     if (const char* fg = std::getenv("DMTK_GPU_MAX_G")) max_g = std::min(max_g, std::max(1, std::atoi(fg)));
     if (mp.kind == kTcM) {
         p.flavor = kMMajor;
-        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, max_g);
-        p.G = tl.G;
-        p.TR = kBM / p.G;
+        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g);
+    } else if (mp.kind == kTcKJ) {
+        p.flavor = kKMajorJ;
+        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g);
+    } else {
+        p.flavor = kKMajorJK;
+        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g);
+    }
+    p.RB = tl.RB;
+    p.BK = tc_bk(p.RB);
+    p.G = tl.G;
+    p.TR = tc_bm(p.RB) / p.G;
+    const long long kstep = static_cast<long long>(p.BK) * p.G;
+    if (mp.kind == kTcM) {
         p.n_ti = (mp.L * mp.I + p.TR - 1) / p.TR;
         p.n_tj = 1;
-        p.stages_per_tile = (mp.R + kBK * p.G - 1) / (kBK * p.G);
+        p.stages_per_tile = (mp.R + kstep - 1) / kstep;
         p.kext = mp.R;
         p.BI = p.TR;
         p.BJ = 1;
     } else if (mp.kind == kTcKJ) {
-        p.flavor = kKMajorJ;
-        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, max_g);
-        p.G = tl.G;
-        p.TR = kBM / p.G;
         p.BI = tl.BI;
         p.BJ = tl.BJ;
         p.n_ti = (mp.I + p.BI - 1) / p.BI;
         p.n_tj = (mp.R + p.BJ - 1) / p.BJ;
-        p.stages_per_tile = (mp.L + kBK * p.G - 1) / (kBK * p.G);
+        p.stages_per_tile = (mp.L + kstep - 1) / kstep;
         p.kext = mp.L;
     } else {
-        p.flavor = kKMajorJK;
-        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, max_g);
-        p.G = tl.G;
-        p.TR = kBM / p.G;
         p.BI = p.TR;
         p.BJ = 1;
         p.n_ti = (mp.I + p.TR - 1) / p.TR;
         p.n_tj = 1;
-        p.n_lc = (mp.L + kBK * p.G - 1) / (kBK * p.G);
+        p.n_lc = (mp.L + kstep - 1) / kstep;
         p.stages_per_tile = mp.R * p.n_lc;
         p.kext = mp.L;
     }
-    // deepest ring (2..4 stages) that fits the 227 KB opt-in shared memory
+    // deepest ring (2..6 stages) that fits the 227 KB opt-in shared memory
     p.stages = 0;
-    for (int st = 4; st >= 2; --st) {
-        const int sm = tc_smem_bytes(mp.nb, mp.tail, p.G, st);
+    static const int max_stages = [] {
+        const char* e = std::getenv("DMTK_GPU_MAX_STAGES");
+        return e ? std::max(2, std::min(6, std::atoi(e))) : 6;
+    }();
+    for (int st = max_stages; st >= 2; --st) {
+        const int sm = tc_smem_bytes(mp.nb, mp.tail, p.G, st, p.RB);
         if (sm > 0 && sm <= 227 * 1024) {
             p.stages = st;
             p.smem = sm;
@@ -427,7 +456,7 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
         max_seg = std::max<int>(max_seg, static_cast<int>((hi - 1) / p.stages_per_tile - lo / p.stages_per_tile + 1));
     }
     p.max_seg = max_seg;
-    mp.ws_doubles = static_cast<long long>(mp.grid) * max_seg * kBM * C;
+    mp.ws_doubles = static_cast<long long>(mp.grid) * max_seg * tc_bm(p.RB) * C;
     return mp;
 }
 
@@ -435,6 +464,7 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
 // (row i, workspace slot) pairs in (CTA, segment, warp, slot) order.
 static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long, long long>>& out) {
     const int wpg = kConsumerWarps / p.G;
+    const int RW = 8 * p.RB, BM = tc_bm(p.RB);
     for (int b = 0; b < grid; ++b) {
         long long lo, hi;
         cta_stage_range(p.total_stages, grid, b, lo, hi);
@@ -444,21 +474,21 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
             const long long seg = tile - t0;
             for (int w = 0; w < kConsumerWarps; ++w) {
                 const int lw = w % wpg;  // every row group writes its own slots
-                const long long base = (static_cast<long long>(b) * p.max_seg + seg) * kBM + kRowsPerWarp * w;
+                const long long base = (static_cast<long long>(b) * p.max_seg + seg) * BM + RW * w;
                 if (p.flavor == kMMajor) {
-                    const long long mrows = p.L * p.I, mbase = tile * p.TR + kRowsPerWarp * lw;
+                    const long long mrows = p.L * p.I, mbase = tile * p.TR + RW * lw;
                     if (p.L == 1) {
-                        for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
+                        for (int r = 0; r < RW && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
                     } else if (mbase < mrows) {
                         const long long ifirst = mbase / p.L;
-                        const long long ilast = std::min(mbase + kRowsPerWarp - 1, mrows - 1) / p.L;
+                        const long long ilast = std::min(mbase + RW - 1, mrows - 1) / p.L;
                         for (long long i = ifirst; i <= ilast; ++i) out.push_back({i, base + (i - ifirst)});
                     }
                 } else if (p.flavor == kKMajorJ) {
                     const long long ti = tile % p.n_ti, tj = tile / p.n_ti;
-                    if (p.BI >= kRowsPerWarp) {
-                        for (int r = 0; r < kRowsPerWarp; ++r) {
-                            const int rho = kRowsPerWarp * lw + r;
+                    if (p.BI >= RW) {
+                        for (int r = 0; r < RW; ++r) {
+                            const int rho = RW * lw + r;
                             const long long i = ti * p.BI + rho % p.BI, j = tj * p.BJ + rho / p.BI;
                             if (i < p.I && j < p.R) out.push_back({i, base + r});
                         }
@@ -469,8 +499,8 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
                         }
                     }
                 } else {
-                    const long long ibase = tile * p.TR + kRowsPerWarp * lw;
-                    for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
+                    const long long ibase = tile * p.TR + RW * lw;
+                    for (int r = 0; r < RW && ibase + r < p.I; ++r) out.push_back({ibase + r, base + r});
                 }
             }
         }
@@ -517,7 +547,7 @@ static CUtensorMap make_map(const double* base, const ModePlan& mp) {
     if (mp.kind == kTcM) {
         const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(mp.L * mp.I), static_cast<cuuint64_t>(mp.R)};
         const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(mp.L * mp.I * 8)};
-        const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(kBK)};
+        const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(mp.tc.BK)};
         const cuuint32_t es[2] = {1, 1};
         // 256-byte L2 promotion only when every column starts 256-byte aligned;
         // otherwise promoted lines straddle tiles that other CTAs stream much
@@ -680,7 +710,7 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
             const int P = C + ((6 - C % 4) % 4);
             const long long bytes = bgen.ext[0] * P * 8;
             const int padded = static_cast<int>((bytes + 127) / 128 * 128);
-            if (bgen.ext[0] >= kBK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
+            if (bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
                 !std::getenv("DMTK_GPU_NO_U0_SMEM")) {
                 mp.tc.u0_pitch = P;
                 mp.tc.smem += padded;
@@ -690,7 +720,7 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         // krp.cpp:53-88), materialised once so a builder's head is one row load
         mp.tc.htab = nullptr;
         mp.tc.hrows = 0;
-        if (bgen.nf >= 2 && bgen.ext[0] >= kBK && bgen.ldu > 0) {
+        if (bgen.nf >= 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0) {
             std::vector<const double*> in;
             std::vector<long long> rows;
             long long hr = 1;
@@ -706,6 +736,14 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         }
 
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
+        static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;
+        if (plan_log)
+            std::fprintf(stderr,
+                         "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
+                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld\n",
+                         mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
+                         mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
+                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows);
         const CUtensorMap map = make_map(X, mp);
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
             fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");

@@ -32,8 +32,10 @@ void launch_fit_cached(const double* U, const double* Mlast, long long rows, int
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s);
 
 // Tensor-core streaming MTTKRP (mttkrp_tc.cuh). nb in [1, 8], tail in
-// {0, 1, 2, 4}; returns false when no instantiation matches.
-int tc_smem_bytes(int nb, int tail, int G, int stages);
+// {0, 1, 2, 4}, rb (row blocks per warp, p.RB) in {2, 3, 4}; returns false /
+// -1 when no instantiation matches.
+bool tc_has_tile(int nb, int tail, int rb);
+int tc_smem_bytes(int nb, int tail, int G, int stages, int rb);
 bool launch_mttkrp_tc(const TcPlan& p, const CUtensorMap& map, int nb, int tail, bool kmajor, int grid, cudaStream_t s);
 
 }  // namespace dmtkg

@@ -19,7 +19,7 @@
 //             = one_step on interior modes (reference mttkrp.cpp:165-242).
 // Work is split stream-K style: the (tile, stage) sequence is cut into
 // equal contiguous ranges, one per CTA; each tile segment a CTA finishes
-// writes one 128-row slot block to the workspace, and a deterministic CSR
+// writes one BM-row slot block to the workspace, and a deterministic CSR
 // reduction (reduce kernel) sums the slots of every output row.
 #pragma once
 
@@ -27,16 +27,19 @@
 
 namespace dmtkg {
 
-constexpr int kBM = 128;  // rows per CTA tile stage (8 consumer warps x 16)
-constexpr int kBK = 32;   // contraction depth per pipeline stage
-constexpr int kConsumerWarps = 8;   // two per SM sub-partition
-constexpr int kRowsPerWarp = kBM / kConsumerWarps;  // 16
-constexpr int kRB = kRowsPerWarp / 8;               // DMMA row blocks per warp
-constexpr int kBuilderWarps = 3;
-constexpr int kThreads = (kConsumerWarps + kBuilderWarps + 1) * 32;
+constexpr int kConsumerWarps = 8;  // two per SM sub-partition
+// Tile shape by RB (DMMA row blocks per consumer warp, 2..4): tile rows
+// 64 * RB at G = 1; contraction indices per stage (and row group) 32 for
+// RB = 2, 16 for taller tiles, so a stage stays 24-32 KB of X.
+__host__ __device__ constexpr int tc_bk(int rb) { return rb == 2 ? 32 : 16; }
+__host__ __device__ constexpr int tc_bm(int rb) { return kConsumerWarps * 8 * rb; }
+// Warp roles: producer, three builders, eight consumers (see mttkrp_tc.cuh).
+// (A setmaxnreg rebalance toward the consumers was measured to add spills,
+// not remove them: ptxas keeps values live across the role split.)
+__host__ __device__ constexpr int tc_builders(int) { return 3; }
+__host__ __device__ constexpr int tc_threads(int rb) { return (kConsumerWarps + tc_builders(rb) + 1) * 32; }
 constexpr int kProducerWarp = 0;
 constexpr int kFirstBuilderWarp = 1;
-constexpr int kFirstConsumerWarp = 1 + kBuilderWarps;
 
 enum Flavor : int { kMMajor = 0, kKMajorJ = 1, kKMajorJK = 2 };
 
@@ -44,21 +47,23 @@ struct TcPlan {
     int flavor;
     int C;                    // rank
     long long L, I, R;        // collapsed view
-    int G;                    // row groups: the 128 tile rows are G groups of TR = 128/G rows,
-                              // each group contracting its own 32-index slice of a stage
-    int TR;                   // tile rows (128 / G)
-    int stages;               // ring depth (2..4)
+    int RB;                   // DMMA row blocks per consumer warp (kernel template, 2..4)
+    int BK;                   // contraction indices per stage and row group (tc_bk(RB))
+    int G;                    // row groups: the BM = tc_bm(RB) tile rows are G groups of TR = BM/G
+                              // rows, each group contracting its own BK-index slice of a stage
+    int TR;                   // tile rows (BM / G)
+    int stages;               // ring depth (2..6)
     int BI, BJ;               // K-major row tile: BI * BJ == TR (kKMajorJK: TR, 1)
     long long n_ti, n_tj;     // tiles along rows (M-major: n_ti = ceil(L*I/TR), n_tj = 1)
-    long long stages_per_tile;  // contraction stages per tile (32 * G indices each)
-    long long n_lc;           // kKMajorJK: l-chunks of 32 * G per j
+    long long stages_per_tile;  // contraction stages per tile (BK * G indices each)
+    long long n_lc;           // kKMajorJK: l-chunks of BK * G per j
     long long total_stages;   // n_ti * n_tj * stages_per_tile
     long long kext;           // extent of the B generator index (R for M-major, L for K-major)
     int max_seg;              // workspace slot blocks per CTA
     int debug;                // experiment switches (0 in production)
     KrpGen bgen;              // B operand rows (index j for M-major, l for K-major)
     KrpGen sgen;              // scale rows: KL over l (M-major), KR over j (K-major)
-    double* ws;               // [grid][max_seg][128][C]
+    double* ws;               // [grid][max_seg][BM][C]
     const double* htab;       // partial KRP of bgen factors 1..nf-1 (hrows x C), or null
     long long hrows;
     int smem;                 // dynamic shared memory bytes

@@ -2,21 +2,26 @@
 // on-the-fly Khatri-Rao B tiles, FP64 tensor-core (DMMA 8x8x4) contraction,
 // fused multi-TTV epilogue. See mttkrp_plan.h for the formulation.
 //
-// Warp roles (352 threads, one CTA per SM, persistent over a stream-K range):
+// Warp roles (384 threads, one CTA per SM, persistent over a stream-K range):
 // The consumers get the highest warp ids: the SMSP arbiter issues
 // highest-wid-first, so DMMA issue wins over builder/producer bookkeeping.
-//   warps 3-10 consumers (two per SM sub-partition, so one warp's loads and
-//              barrier waits hide behind the other's DMMAs): 16 tile rows
-//              each x all C columns. Columns in
-//              groups of 8 run on DMMA; the C % 8 remainder ("tail") runs on
-//              DFMA so no tensor-core work is wasted on padding.
-//   warps 1-2  builders, alternating stages: write the stage's B tile (32
-//              KRP rows x C) into shared memory in DMMA fragment order, one
-//              multiply per entry (cached head partial x fastest factor row:
-//              the paper's reuse scheme, Alg. 1, krp.cpp:53-88).
+//   warps 4-11 consumers (two per SM sub-partition, so one warp's loads and
+//              barrier waits hide behind the other's DMMAs): RW = 8 * RB tile
+//              rows each x all C columns. Columns in groups of 8 run on DMMA;
+//              a C % 8 remainder of 1-2 ("tail") runs on DFMA.
+//   warps 1-3  builders: write the stage's B tile (BK KRP rows x C per row
+//              group) into shared memory in DMMA fragment order, one multiply
+//              per entry (head-table row x fastest factor row: the paper's
+//              reuse scheme, Alg. 1, krp.cpp:53-88).
 //   warp 0     producer: one elected lane issues the TMA box loads.
-// Per stage: full barrier (TMA bytes + 1 builder arrival), empty barrier
-// (8 consumer arrivals).
+// Per stage: full barrier (TMA bytes + one arrival per builder item), empty
+// barrier (8 consumer arrivals).
+//
+// Tile shape (template RB): BM = 64 * RB rows x BK contraction indices per
+// stage, BK = 32 for RB = 2 (128-row tiles) and 16 for RB = 3, 4 (192- and
+// 256-row tiles): a stage is 24-32 KB of X either way. Taller tiles share
+// one B row among more X rows (less builder work and fewer shared-memory
+// B fragment reads per byte of X) and fit extents like 180 in one tile.
 //
 // The A tile arrives through 128-byte-swizzled TMA boxes; the k index a
 // DMMA fragment lane reads is permuted (kperm) so that all fragment loads
@@ -27,16 +32,20 @@
 
 namespace dmtkg {
 
-template <int NB, int TAIL>
+template <int NB, int TAIL, int RB>
 struct TcCfg {
     static constexpr int CP = 8 * NB + TAIL;
-    static constexpr int MAX_STAGES = 4;
-    static constexpr int A_BYTES = kBM * kBK * 8;  // one stage of X: 32 KB
-    static constexpr int BMAIN = kBK * 8 * NB;     // doubles per group, DMMA fragments
-    static constexpr int BTAIL = kBK * TAIL;       // doubles per group, DFMA tail columns
+    static constexpr int RW = 8 * RB;                 // rows per consumer warp
+    static constexpr int BM = kConsumerWarps * RW;    // tile rows at G = 1
+    static constexpr int BK = tc_bk(RB);              // contraction indices per stage (per row group)
+    static constexpr int KS = BK / 4;                 // DMMA k4-steps per stage
+    static constexpr int MAX_STAGES = 6;
+    static constexpr int A_BYTES = BM * BK * 8;       // one stage of X: 24-32 KB
+    static constexpr int BMAIN = BK * 8 * NB;         // doubles per group, DMMA fragments
+    static constexpr int BTAIL = BK * TAIL;           // doubles per group, DFMA tail columns
     static constexpr int B_BYTES = ((BMAIN + BTAIL) * 8 + 1023) / 1024 * 1024;  // one row group
     static constexpr int EPI_LD = CP + 1;
-    static constexpr int EPI_BYTES = ((kConsumerWarps * kRowsPerWarp * EPI_LD * 8) + 1023) / 1024 * 1024;
+    static constexpr int EPI_BYTES = ((kConsumerWarps * RW * EPI_LD * 8) + 1023) / 1024 * 1024;
     static constexpr int BAR_BYTES = 2 * MAX_STAGES * 8;
     // everything but the ring; the host adds stages * (A_BYTES + G * B_BYTES)
     static constexpr int FIXED = EPI_BYTES + BAR_BYTES + 1024;
@@ -75,10 +84,15 @@ struct StageCursor {
     }
 };
 
-template <int NB, int TAIL, bool KMAJ>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NB, int TAIL, bool KMAJ, int RB>
+__global__ void __launch_bounds__(tc_threads(RB), 1)
     mttkrp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcPlan p) {
-    using Cfg = TcCfg<NB, TAIL>;
+    using Cfg = TcCfg<NB, TAIL, RB>;
+    constexpr int RW = Cfg::RW;
+    constexpr int BK = Cfg::BK;
+    constexpr int KS = Cfg::KS;
+    constexpr int kBuilderWarps = tc_builders(RB);
+    constexpr int kFirstConsumerWarp = kFirstBuilderWarp + kBuilderWarps;
     const int STAGES = p.stages;
     const int G = p.G;
     const int GB_BYTES = G * Cfg::B_BYTES;  // B tile of one stage (all row groups)
@@ -128,36 +142,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mbar_arrive_expect_tx_a(full_a + 8 * slot, Cfg::A_BYTES);
                 const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
-                const int gshift = 4 - __ffs(G);  // log2(8 / G): consumer warps (and 16-row boxes) per group
                 if (!KMAJ) {
-                    // 8 boxes {16 m, 32 j}: box b is row group b >> gshift,
-                    // rows 16 * (b & (8/G - 1)) of the group's TR-row tile
+                    // BM / 16 boxes {16 m, BK j} of 128 * BK bytes: group gi's
+                    // boxes cover rows 16 bb of its TR-row tile at j0 + BK gi
                     const int m0 = static_cast<int>(tile * p.TR);
-                    const int j0 = static_cast<int>(st * kBK * G);
-#pragma unroll
-                    for (int b = 0; b < 8; ++b)
-                        tma_load_2d(dst + b * 4096, &tmap, full_a + 8 * slot, m0 + 16 * (b & ((1 << gshift) - 1)),
-                                    j0 + kBK * (b >> gshift), pol);
+                    const int j0 = static_cast<int>(st * BK * G);
+                    const int bpg = p.TR / 16;
+                    uint32_t d = dst;
+                    for (int gi = 0; gi < G; ++gi)
+                        for (int bb = 0; bb < bpg; ++bb, d += 128 * BK)
+                            tma_load_2d(d, &tmap, full_a + 8 * slot, m0 + 16 * bb, j0 + BK * gi, pol);
                 } else {
                     long long ti, tj, j, l0;
                     if (p.flavor == kKMajorJ) {
                         tj = div_nn(tile, p.n_ti);
                         ti = tile - tj * p.n_ti;
-                        l0 = st * kBK * G;
+                        l0 = st * BK * G;
                         j = tj * p.BJ;
                     } else {
                         ti = tile;
                         j = div_nn(st, p.n_lc);
-                        l0 = (st - j * p.n_lc) * kBK * G;
+                        l0 = (st - j * p.n_lc) * BK * G;
                     }
+                    // per group: BK / 16 boxes {16 l, BI, BJ} of TR * 128 bytes
                     const int gbytes = Cfg::A_BYTES / G;
                     for (int gi = 0; gi < G; ++gi) {
 #pragma unroll
-                            for (int h = 0; h < 2; ++h)
-                                tma_load_3d(dst + gi * gbytes + h * (gbytes / 2), &tmap, full_a + 8 * slot,
-                                            static_cast<int>(l0 + kBK * gi + 16 * h), static_cast<int>(ti * p.BI),
-                                            static_cast<int>(j), pol);
-                        }
+                        for (int h = 0; h < BK / 16; ++h)
+                            tma_load_3d(dst + gi * gbytes + h * (gbytes / (BK / 16)), &tmap, full_a + 8 * slot,
+                                        static_cast<int>(l0 + BK * gi + 16 * h), static_cast<int>(ti * p.BI),
+                                        static_cast<int>(j), pol);
+                    }
                     }
                 }
             }
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int t = lane & 3;
         const KrpGen& Gen = p.bgen;
         const long long e0 = Gen.ext[0];
-        const bool fast = e0 >= kBK;
+        const bool fast = e0 >= BK;
         const int C = p.C;
         const long long kext = p.kext;
         const double* __restrict__ U0 = Gen.U[0];
@@ -213,9 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 long long kbase, jx = -1;
                 if (KMAJ && p.flavor == kKMajorJK) {
                     jx = div_nn(cur.st, p.n_lc);
-                    kbase = (cur.st - jx * p.n_lc) * kBK * G + kBK * gi;
+                    kbase = (cur.st - jx * p.n_lc) * BK * G + BK * gi;
                 } else {
-                    kbase = cur.st * kBK * G + kBK * gi;
+                    kbase = cur.st * BK * G + BK * gi;
                 }
                 long long q0 = 0;
                 int r0 = 0;
@@ -269,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 double* Bm = reinterpret_cast<double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
                 double* Bt = Bm + Cfg::BMAIN;
                 // wide ranks build the item in two chunks of k4-steps (registers)
-                constexpr int NCH = NB > 4 ? 2 : 1;
-                constexpr int SPC = 8 / NCH;
+                constexpr int NCH = NB > 4 && KS == 8 ? 2 : 1;
+                constexpr int SPC = KS / NCH;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     double u[SPC][NB];
@@ -363,36 +378,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int w = warp - kFirstConsumerWarp;
     const int wpg = kConsumerWarps / G;  // consumer warps per row group
     const int gi = w / wpg;              // this warp's row group (its contraction slice)
-    const int lw = w - gi * wpg;         // warp within the group: rows 16 lw .. 16 lw + 15
+    const int lw = w - gi * wpg;         // warp within the group: rows RW lw .. RW lw + RW - 1
     const int gl = lane >> 2;  // fragment row / B column
     const int tl = lane & 3;   // fragment k / D column pair
-    // per-lane A fragment offsets (bytes within a stage), see kperm
-    uint32_t aoff[4];
+    // per-lane A fragment offsets (bytes within a stage), see kperm.
+    // M-major: row block rb of this warp is stage row rho = RW w + 8 rb, in
+    // box rho / 16 (128 * BK bytes each) at m = rho % 16; k = 8 (s >> 1) +
+    // 2 t + (s & 1), so the box row is k & 7 = 2 t + (s & 1) of k-octet s >> 1.
+    // K-major: x = s & 3; k & 15 = 8 (t >> 1) + (t & 1) + 2 (s & 3).
+    uint32_t aoff[KMAJ ? 4 : 2 * RB];
+    if (!KMAJ) {
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        if (!KMAJ) {
-            // x = 2 * (s & 1) + (rb & 1); box row k & 7 = 2 t + (s & 1)
-            const uint32_t kr7 = 2 * tl + (x >> 1);
-            const uint32_t mm = 8 * (x & 1) + gl;
-            aoff[x] = kr7 * 128 + ((mm * 8) ^ (kr7 << 4));
-        } else {
-            // x = s & 3; k & 15 = 8 (t >> 1) + (t & 1) + 2 (s & 3)
+        for (int rb = 0; rb < RB; ++rb) {
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const uint32_t rho = RW * w + 8 * rb;
+                const uint32_t kr7 = 2 * tl + x;
+                const uint32_t mm = (rho & 15u) + gl;
+                aoff[2 * rb + x] = (rho >> 4) * (128 * BK) + kr7 * 128 + ((mm * 8) ^ (kr7 << 4));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
             const uint32_t kk = 8 * (tl >> 1) + (tl & 1) + 2 * x;
             aoff[x] = (kk * 8) ^ (static_cast<uint32_t>(gl) << 4);
         }
     }
 
-    double acc[kRB][NB][2];
-    double tacc[kRB][TAIL > 0 ? TAIL : 1];
+    double acc[RB][NB][2];
+    // tail accumulators split by k4-step parity: two independent DFMA chains
+    double tacc[2][RB][TAIL > 0 ? TAIL : 1];
 #pragma unroll
-    for (int rb = 0; rb < kRB; ++rb) {
+    for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
 #pragma unroll
-        for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) tacc[rb][tc] = 0.0;
+        for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) tacc[0][rb][tc] = tacc[1][rb][tc] = 0.0;
     }
 
-    double* Pw = sEpi + w * kRowsPerWarp * Cfg::EPI_LD;
+    double* Pw = sEpi + w * RW * Cfg::EPI_LD;
     int seg = 0;
 
     // Fragments of one k4-step pair, double-buffered in registers: the loads
@@ -401,12 +426,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of the current one, so the tensor pipe sees no stage-boundary bubble.
     struct Frag {
         double2 bv[NB];
-        double a[2][kRB];
+        double a[2][RB];
         double bt[2][TAIL > 0 ? TAIL : 1];
     };
-    const uint32_t a_warp = KMAJ ? static_cast<uint32_t>(gi * (Cfg::A_BYTES / G) + (kRowsPerWarp * lw + gl) * 128)
-                                 : static_cast<uint32_t>(w * 4096);
-    const uint32_t a_box = KMAJ ? static_cast<uint32_t>(Cfg::A_BYTES / 2 / G) : 0u;
+    const uint32_t a_warp = KMAJ ? static_cast<uint32_t>(gi * (Cfg::A_BYTES / G) + (RW * lw + gl) * 128) : 0u;
+    const uint32_t a_box = KMAJ ? static_cast<uint32_t>(Cfg::A_BYTES / G / (BK / 16)) : 0u;
     auto load = [&](Frag& f, int sl, int s2) {
         const unsigned char* As = sA + sl * Cfg::A_BYTES;
         const double* Bm = reinterpret_cast<const double*>(sB + sl * GB_BYTES + gi * Cfg::B_BYTES);
@@ -417,8 +441,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sub = 0; sub < 2; ++sub) {
             const int s = 2 * s2 + sub;
 #pragma unroll
-            for (int rb = 0; rb < kRB; ++rb) {
-                const uint32_t off = !KMAJ ? a_warp + (s >> 1) * 1024 + aoff[2 * (s & 1) + (rb & 1)]
+            for (int rb = 0; rb < RB; ++rb) {
+                const uint32_t off = !KMAJ ? (s >> 1) * 1024 + aoff[2 * rb + (s & 1)]
                                            : a_warp + (s >> 2) * a_box + 8 * rb * 128 + aoff[s & 3];
                 f.a[sub][rb] = *reinterpret_cast<const double*>(As + off);
             }
@@ -433,17 +457,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
 #pragma unroll
-            for (int rb = 0; rb < kRB; ++rb) {
+            for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb)
                     dmma_8x8x4(acc[rb][nb][0], acc[rb][nb][1], f.a[sub][rb], sub ? f.bv[nb].y : f.bv[nb].x);
             }
             if (TAIL > 0) {
 #pragma unroll
-                for (int rb = 0; rb < kRB; ++rb) {
+                for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
                     for (int tc = 0; tc < TAIL; ++tc)
-                        tacc[rb][tc] = fma(f.a[sub][rb], f.bt[sub][tc], tacc[rb][tc]);
+                        tacc[sub][rb][tc] = fma(f.a[sub][rb], f.bt[sub][tc], tacc[sub][rb][tc]);
                 }
             }
         }
@@ -453,153 +477,174 @@ __global__ void __launch_bounds__(kThreads, 1)
     // groups that pushes the kernel past its register budget (spills cost
     // more than the bubble), so wide ranks load per pair instead.
     constexpr bool kPrefetch = NB <= 3;
-    StageCursor cur;
-    cur.init(lo, spt);
+    // Segments (the stages of one tile inside this CTA's range) run as an
+    // int-counted inner loop: per-stage bookkeeping is a ring-slot step only.
+    int slot = 0;
+    uint32_t ph = 0;
+    long long tile = lo / spt;
+    long long st0 = lo - tile * spt;
     Frag f0, f1;
     if (kPrefetch && lo < hi) {
-        mbar_wait_a(full_a + 8 * cur.slot, cur.ph);
-        load(f0, cur.slot, 0);
+        mbar_wait_a(full_a, 0u);
+        load(f0, 0, 0);
     }
-    for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
-        const int slot = cur.slot;
-        const long long tile = cur.tile;
-        if (kPrefetch) {
-            StageCursor nxt = cur;
-            nxt.next(spt, STAGES);
-            const bool has_next = gs + 1 < hi;
+    for (long long gs = lo; gs < hi; ++tile, st0 = 0, ++seg) {
+        const int nseg = static_cast<int>(spt - st0 < hi - gs ? spt - st0 : hi - gs);
+        gs += nseg;
+        const bool more = gs < hi;  // another segment follows
+        for (int k = 0; k < nseg; ++k) {
+            const int nslot = slot + 1 == STAGES ? 0 : slot + 1;
+            const uint32_t nph = nslot == 0 ? ph ^ 1u : ph;
+            if (kPrefetch) {
+                const bool has_next = more || k + 1 < nseg;
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                Frag& cf = (s2 & 1) ? f1 : f0;
-                Frag& nf = (s2 & 1) ? f0 : f1;
-                if (s2 < 3) {
-                    load(nf, slot, s2 + 1);
-                } else if (has_next) {
-                    mbar_wait_a(full_a + 8 * nxt.slot, nxt.ph);
-                    load(nf, nxt.slot, 0);
+                for (int s2 = 0; s2 < KS / 2; ++s2) {
+                    Frag& cf = (s2 & 1) ? f1 : f0;
+                    Frag& nf = (s2 & 1) ? f0 : f1;
+                    if (s2 < KS / 2 - 1) {
+                        load(nf, slot, s2 + 1);
+                    } else {
+                        // unconditional load keeps the fragment dataflow
+                        // branch-free; past the range end it re-reads the
+                        // current (still owned) slot and is discarded
+                        if (has_next) mbar_wait_a(full_a + 8 * nslot, nph);
+                        load(nf, has_next ? nslot : slot, 0);
+                    }
+                    compute(cf);
                 }
-                compute(cf);
-            }
-        } else {
-            mbar_wait_a(full_a + 8 * slot, cur.ph);
+            } else {
+                mbar_wait_a(full_a + 8 * slot, ph);
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                load(f0, slot, s2);
-                compute(f0);
+                for (int s2 = 0; s2 < KS / 2; ++s2) {
+                    load(f0, slot, s2);
+                    compute(f0);
+                }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(empty_a + 8 * slot);
+            slot = nslot;
+            ph = nph;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_a(empty_a + 8 * slot);
-
-        const bool seg_end = (gs + 1 == hi) || (cur.st + 1 == spt);
-        if (!seg_end) continue;
         if (p.debug & 8) {  // experiment: drop the epilogue entirely
 #pragma unroll
-            for (int rb = 0; rb < kRB; ++rb)
+            for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
-            ++seg;
             continue;
         }
 
         // ------------------------------------------------- epilogue (warp-local)
+        // Rows are finished in chunks of EC (a divisor of RW, at most 16) so
+        // the scale loads in flight stay within the register budget at RW =
+        // 32. The accumulators are re-zeroed only after the epilogue (dead,
+        // not live zeros, meanwhile).
         constexpr int LD = Cfg::EPI_LD;
+        constexpr int EC = RW % 16 == 0 ? 16 : 8;
+        static_assert(RW % EC == 0, "epilogue chunk must divide the warp's rows");
 #pragma unroll
-        for (int rb = 0; rb < kRB; ++rb) {
+        for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
                 Pw[(8 * rb + gl) * LD + 8 * nb + 2 * tl] = acc[rb][nb][0];
                 Pw[(8 * rb + gl) * LD + 8 * nb + 2 * tl + 1] = acc[rb][nb][1];
-                acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
             }
+            if (TAIL > 0) {
 #pragma unroll
-            for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) {
-                if (TAIL > 0) {
-                    double v = tacc[rb][tc];
+                for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) {
+                    double v = tacc[0][rb][tc] + tacc[1][rb][tc];
                     v += __shfl_xor_sync(0xffffffffu, v, 1);
                     v += __shfl_xor_sync(0xffffffffu, v, 2);
                     if (tl == 0) Pw[(8 * rb + gl) * LD + 8 * NB + tc] = v;
                 }
-                tacc[rb][tc] = 0.0;
             }
         }
         __syncwarp();
         const int C = p.C;
-        double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * kBM + kRowsPerWarp * w) * C;
+        double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * Cfg::BM + RW * w) * C;
         for (int c = lane; c < C; c += 32) {
             if (!KMAJ) {
                 const long long mrows = p.L * p.I;
-                const long long mbase = tile * p.TR + kRowsPerWarp * lw;
+                const long long mbase = tile * p.TR + RW * lw;
                 if (p.L == 1) {
-                    for (int r = 0; r < kRowsPerWarp && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
-                } else if (mbase + kRowsPerWarp <= mrows && p.L >= kRowsPerWarp && p.sgen.nf == 1) {
-                    // common multi-TTV case: 16 full rows, l wraps at most once,
+                    for (int r = 0; r < RW && mbase + r < mrows; ++r) wsb[r * C + c] = Pw[r * LD + c];
+                } else if (mbase + RW <= mrows && p.L >= RW && p.sgen.nf == 1) {
+                    // common multi-TTV case: RW full rows, l wraps at most once,
                     // a single (materialised or one-input) scale factor
                     const long long ifirst = div_nn(mbase, p.L);
                     const int l0 = static_cast<int>(mbase - ifirst * p.L);
                     const int rw = static_cast<int>(p.L) - l0;  // first row of the next i
                     const double* sbase = p.sgen.U[0] + c;
                     const long long ldu = p.sgen.ldu;
-                    double sc[kRowsPerWarp];
-#pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r) {
-                        const int l = r < rw ? l0 + r : l0 + r - static_cast<int>(p.L);
-                        sc[r] = __ldg(sbase + l * ldu);
-                    }
                     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r) {
-                        const double v = Pw[r * LD + c] * sc[r];
-                        if (r < rw) s0 += v; else s1 += v;
+                    for (int r0 = 0; r0 < RW; r0 += EC) {
+                        double sc[EC];
+#pragma unroll
+                        for (int r = 0; r < EC; ++r) {
+                            const int rr = r0 + r;
+                            const int l = rr < rw ? l0 + rr : l0 + rr - static_cast<int>(p.L);
+                            sc[r] = __ldg(sbase + l * ldu);
+                        }
+#pragma unroll
+                        for (int r = 0; r < EC; ++r) {
+                            const double v = Pw[(r0 + r) * LD + c] * sc[r];
+                            if (r0 + r < rw) s0 += v; else s1 += v;
+                        }
                     }
                     wsb[c] = s0;
-                    if (rw < kRowsPerWarp) wsb[C + c] = s1;
+                    if (rw < RW) wsb[C + c] = s1;
                 } else if (mbase < mrows) {
                     // general case: partial rows, short L, multi-factor scales
                     const long long ifirst = div_nn(mbase, p.L);
                     const long long l0 = mbase - ifirst * p.L;
-                    double sc[kRowsPerWarp];
-#pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r) {
-                        long long l = l0 + r;
-                        if (l >= p.L) l = p.L >= kRowsPerWarp ? l - p.L : l - p.L * div_nn(l, p.L);
-                        sc[r] = (mbase + r < mrows) ? krp_scale(p.sgen, l, c) : 0.0;
-                    }
                     long long l = l0;
                     long long cur = ifirst;
                     double sum = 0.0;
+                    for (int r0 = 0; r0 < RW && mbase + r0 < mrows; r0 += EC) {
+                        double sc[EC];
 #pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r, ++l) {
-                        if (mbase + r >= mrows) break;
-                        if (l == p.L) {
-                            wsb[(cur - ifirst) * C + c] = sum;
-                            ++cur;
-                            sum = 0.0;
-                            l = 0;
+                        for (int r = 0; r < EC; ++r) {
+                            long long lr = l0 + r0 + r;
+                            if (lr >= p.L) lr = lr - p.L * div_nn(lr, p.L);
+                            sc[r] = (mbase + r0 + r < mrows) ? krp_scale(p.sgen, lr, c) : 0.0;
                         }
-                        sum += Pw[r * LD + c] * sc[r];
+#pragma unroll
+                        for (int r = 0; r < EC; ++r, ++l) {
+                            if (mbase + r0 + r >= mrows) break;
+                            if (l == p.L) {
+                                wsb[(cur - ifirst) * C + c] = sum;
+                                ++cur;
+                                sum = 0.0;
+                                l = 0;
+                            }
+                            sum += Pw[(r0 + r) * LD + c] * sc[r];
+                        }
                     }
                     wsb[(cur - ifirst) * C + c] = sum;
                 }
             } else if (p.flavor == kKMajorJ) {
                 const long long tj = div_nn(tile, p.n_ti);
                 const long long ti = tile - tj * p.n_ti;
-                if (p.BI >= kRowsPerWarp) {
-                    double sc[kRowsPerWarp];
-                    bool ok[kRowsPerWarp];
+                if (p.BI >= RW) {
 #pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r) {
-                        const int rho = kRowsPerWarp * lw + r;
-                        const long long i = ti * p.BI + rho % p.BI;
-                        const long long j = tj * p.BJ + rho / p.BI;
-                        ok[r] = i < p.I && j < p.R;
-                        sc[r] = ok[r] ? krp_scale(p.sgen, j, c) : 0.0;
+                    for (int r0 = 0; r0 < RW; r0 += EC) {
+                        double sc[EC];
+                        bool ok[EC];
+#pragma unroll
+                        for (int r = 0; r < EC; ++r) {
+                            const int rho = RW * lw + r0 + r;
+                            const long long i = ti * p.BI + rho % p.BI;
+                            const long long j = tj * p.BJ + rho / p.BI;
+                            ok[r] = i < p.I && j < p.R;
+                            sc[r] = ok[r] ? krp_scale(p.sgen, j, c) : 0.0;
+                        }
+#pragma unroll
+                        for (int r = 0; r < EC; ++r)
+                            if (ok[r]) wsb[(r0 + r) * C + c] = Pw[(r0 + r) * LD + c] * sc[r];
                     }
-#pragma unroll
-                    for (int r = 0; r < kRowsPerWarp; ++r)
-                        if (ok[r]) wsb[r * C + c] = Pw[r * LD + c] * sc[r];
                 } else {
-                    const int njl = kRowsPerWarp / p.BI;
-                    const int jl0 = (kRowsPerWarp * lw) / p.BI;
+                    const int njl = RW / p.BI;
+                    const int jl0 = (RW * lw) / p.BI;
                     for (int il = 0; il < p.BI; ++il) {
                         const long long i = ti * p.BI + il;
                         if (i >= p.I) continue;
@@ -612,12 +657,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                const long long ibase = tile * p.TR + kRowsPerWarp * lw;
-                for (int r = 0; r < kRowsPerWarp && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
+                const long long ibase = tile * p.TR + RW * lw;
+                for (int r = 0; r < RW && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
             }
         }
         __syncwarp();
-        ++seg;
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
+#pragma unroll
+            for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) tacc[0][rb][tc] = tacc[1][rb][tc] = 0.0;
+        }
     }
 }
 

@@ -1,0 +1,28 @@
+"""Every tile shape of the streaming MTTKRP kernel (rows per warp RB = 2, 3, 4;
+row groups G = 1, 2, 4) against a float64 numpy contraction, on shapes with
+ragged tiles, short contractions and multi-TTV epilogues on both flavors.
+
+The planner picks one shape per call, so each (RB, G) is forced through the
+developer switches DMTK_GPU_FORCE_RB / DMTK_GPU_FORCE_G in a subprocess
+(they are read once per process). Tolerance: relative Frobenius <= 1e-12
+(reference test_mttkrp.cpp:134).
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHAPES = ["10x12x14:20", "16x18x20:25", "40x40x12x8:20", "30x20x10x8:16", "64x2x96:3", "130x66x34:9", "6x10x4x2x2x4:17"]
+
+
+@pytest.mark.parametrize("rb", [2, 3, 4])
+@pytest.mark.parametrize("g", [1, 2, 4])
+def test_forced_tile_shape(rb, g):
+    env = dict(os.environ, DMTK_GPU_FORCE_RB=str(rb), DMTK_GPU_FORCE_G=str(g))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *SHAPES], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
