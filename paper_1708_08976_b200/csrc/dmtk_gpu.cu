@@ -251,6 +251,9 @@ enum Kind : int { kTcM = 0, kTcKJ = 1, kTcKJK = 2, kGeneric = 3 };
 struct ModePlan {
     int kind = kGeneric;
     long long L = 1, I = 1, R = 1;
+    long long out_rows = 1;  // rows of the result (I, or L / R for a swapped boundary view)
+    int variant = 0;         // CSR cache key part: boundary 2-step split point s (swap), else 0
+    double cost = 1e300;     // modelled cost (relative padded work), for choosing among views
     int BI = 128, BJ = 1;
     int nb = 0, tail = 0;
     int grid = 1;
@@ -308,7 +311,7 @@ static double tile_cost(int RB, int G) {
 }
 
 static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int nb, int tail,
-                             int max_g_rb2) {
+                             int max_g_rb2, double* cost_out) {
     Tiling best{2, 1, 128, 1};
     double best_cost = 1e300;
     static const int force_g = [] {
@@ -350,16 +353,26 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
             }
         }
     }
+    *cost_out = best_cost;
     return best;
 }
 
 // Flavor for (mode, resolved algorithm, order) on the collapsed view.
+static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms);
+
 static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, int kind_req, int sms) {
-    ModePlan mp;
     const int N = static_cast<int>(dims.size());
-    mp.L = prod(dims, 0, mode);
-    mp.I = dims[mode];
-    mp.R = prod(dims, mode + 1, N);
+    return plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C, kind_req, 0, sms);
+}
+
+// Plan on the collapsed view X(l, i, j); swap selects the boundary 2-step
+// epilogue (mttkrp_plan.h): output rows L (M-major) or R (K-major).
+static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms) {
+    ModePlan mp;
+    mp.L = L;
+    mp.I = I;
+    mp.R = R;
+    mp.out_rows = I;
     int nb = 0, tail = 0;
     const bool rank_ok = tail_of(C, nb, tail);
     mp.nb = nb;
@@ -386,20 +399,23 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
     p.L = mp.L;
     p.I = mp.I;
     p.R = mp.R;
+    p.swap = swap;
+    if (swap) mp.out_rows = kind_req == kTcM ? mp.L : mp.R;
     Tiling tl;
+    double tcost = 1e300;
     int max_g = 1;  // 128-row tiles: row groups whose B tiles still leave room for a 2-stage ring
     for (int g : {2, 4})
         if (tc_smem_bytes(mp.nb, mp.tail, g, 2, 2) <= 227 * 1024) max_g = g;
     if (const char* fg = std::getenv("DMTK_GPU_MAX_G")) max_g = std::min(max_g, std::max(1, std::atoi(fg)));
     if (mp.kind == kTcM) {
         p.flavor = kMMajor;
-        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g);
+        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g, &tcost);
     } else if (mp.kind == kTcKJ) {
         p.flavor = kKMajorJ;
-        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g);
+        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g, &tcost);
     } else {
         p.flavor = kKMajorJK;
-        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g);
+        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g, &tcost);
     }
     p.RB = tl.RB;
     p.BK = tc_bk(p.RB);
@@ -457,6 +473,8 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
     }
     p.max_seg = max_seg;
     mp.ws_doubles = static_cast<long long>(mp.grid) * max_seg * tc_bm(p.RB) * C;
+    // one tile epilogue costs about one stage
+    mp.cost = tcost * static_cast<double>(p.stages_per_tile + 1) / static_cast<double>(p.stages_per_tile);
     return mp;
 }
 
@@ -475,7 +493,26 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
             for (int w = 0; w < kConsumerWarps; ++w) {
                 const int lw = w % wpg;  // every row group writes its own slots
                 const long long base = (static_cast<long long>(b) * p.max_seg + seg) * BM + RW * w;
-                if (p.flavor == kMMajor) {
+                if (p.flavor == kMMajor && p.swap) {
+                    const long long mrows = p.L * p.I, mbase = tile * p.TR + RW * lw;
+                    if (mbase < mrows) {
+                        const long long l0 = mbase % p.L;
+                        const int nslot = p.L >= RW ? RW : static_cast<int>(p.L);
+                        for (int q = 0; q < nslot && mbase + q < mrows; ++q) out.push_back({(l0 + q) % p.L, base + q});
+                    }
+                } else if (p.flavor == kKMajorJ && p.swap) {
+                    const long long ti = tile % p.n_ti, tj = tile / p.n_ti;
+                    (void)ti;
+                    if (p.BI >= RW) {
+                        const long long j = tj * p.BJ + (RW * lw) / p.BI;
+                        if (j < p.R) out.push_back({j, base});
+                    } else {
+                        for (int q = 0; q < RW / p.BI; ++q) {
+                            const long long j = tj * p.BJ + (RW * lw) / p.BI + q;
+                            if (j < p.R) out.push_back({j, base + q});
+                        }
+                    }
+                } else if (p.flavor == kMMajor) {
                     const long long mrows = p.L * p.I, mbase = tile * p.TR + RW * lw;
                     if (p.L == 1) {
                         for (int r = 0; r < RW && mbase + r < mrows; ++r) out.push_back({mbase + r, base + r});
@@ -520,10 +557,10 @@ static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& m
         tc_slots(mp.tc, mp.grid, pairs);
     }
     auto plan = std::make_unique<CsrPlan>();
-    plan->rows = mp.I;
-    std::vector<long long> rowptr(mp.I + 1, 0), slots(pairs.size());
+    plan->rows = mp.out_rows;
+    std::vector<long long> rowptr(mp.out_rows + 1, 0), slots(pairs.size());
     for (auto& pr : pairs) ++rowptr[pr.first + 1];
-    for (long long i = 0; i < mp.I; ++i) rowptr[i + 1] += rowptr[i];
+    for (long long i = 0; i < mp.out_rows; ++i) rowptr[i + 1] += rowptr[i];
     std::vector<long long> fill(rowptr.begin(), rowptr.end() - 1);
     for (auto& pr : pairs) slots[fill[pr.first]++] = pr.second;  // stable: keeps (CTA, seg, warp) order
     plan->rowptr.ensure(rowptr.size());
@@ -601,6 +638,8 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
     int vmode = mode;
     KrpGen bgen{}, sgen{};
     int kind;
+    ModePlan pre;  // plan chosen while routing (boundary 1-step / 2-step views)
+    bool have_pre = false;
     const double* ones = ctx.ones.p;
 
     if (algo == DMTK_GPU_BASELINE) {
@@ -643,14 +682,38 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
             sgen = make_gen(vdims, 0, 0, nullptr, C, ones);
         }
     } else if (algo == DMTK_GPU_ONE_STEP) {
-        if (mode == 0) {
-            kind = kTcM;
-            bgen = make_gen(dims, 1, N, dU, C, ones);
-            sgen = make_gen(dims, 0, 0, dU, C, ones);
-        } else if (mode == N - 1) {
-            kind = kTcKJ;
-            bgen = make_gen(dims, 0, mode, dU, C, ones);
-            sgen = make_gen(dims, N, N, dU, C, ones);
+        if (mode == 0 || mode == N - 1) {
+            // 1-step on the boundary mode, or the boundary 2-step (swap) on a
+            // re-collapsed view when a short extent would leave tile rows empty
+            const bool m0 = mode == 0;
+            kind = m0 ? kTcM : kTcKJ;
+            pre = plan_mode(dims, mode, C, kind, ctx.sms);
+            have_pre = true;
+            int best_s = 0;
+            static const bool no_swap = std::getenv("DMTK_GPU_NO_SWAP") != nullptr;
+            if (pre.kind != kGeneric && !no_swap) {
+                for (int sp = 1; sp <= N - 2; ++sp) {
+                    ModePlan cand = m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM, 1,
+                                                   ctx.sms)
+                                       : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C, kTcKJ, 1,
+                                                   ctx.sms);
+                    if (cand.kind != kGeneric && cand.cost < pre.cost * 0.97) {
+                        pre = cand;
+                        best_s = sp;
+                    }
+                }
+            }
+            pre.variant = best_s;
+            if (best_s == 0) {
+                bgen = m0 ? make_gen(dims, 1, N, dU, C, ones) : make_gen(dims, 0, mode, dU, C, ones);
+                sgen = m0 ? make_gen(dims, 0, 0, dU, C, ones) : make_gen(dims, N, N, dU, C, ones);
+            } else if (m0) {
+                bgen = make_gen(dims, best_s + 1, N, dU, C, ones);
+                sgen = make_gen(dims, 1, best_s + 1, dU, C, ones);
+            } else {
+                bgen = make_gen(dims, 0, best_s, dU, C, ones);
+                sgen = make_gen(dims, best_s, N - 1, dU, C, ones);
+            }
         } else {
             kind = kTcKJK;
             bgen = make_gen(dims, 0, mode, dU, C, ones);
@@ -689,9 +752,9 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         }
     }
 
-    ModePlan mp = plan_mode(vdims, vmode, C, kind, ctx.sms);
+    ModePlan mp = have_pre ? pre : plan_mode(vdims, vmode, C, kind, ctx.sms);
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
-    CsrPlan& csr = csr_for(t, plan_mode_key * 8 + (kind == kTcKJ ? 1 : 0), C, mp, ctx);
+    CsrPlan& csr = csr_for(t, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0), C, mp, ctx);
     ctx.ws.ensure(static_cast<size_t>(mp.ws_doubles));
     if (mp.kind == kGeneric) {
         // the generic kernel indexes KL over l and KR over j directly
@@ -740,17 +803,17 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         if (plan_log)
             std::fprintf(stderr,
                          "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
-                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld\n",
+                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f\n",
                          mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
                          mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
-                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows);
+                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost);
         const CUtensorMap map = make_map(X, mp);
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
             fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
         check_launch("mttkrp_tc");
     }
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
-    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.I, C, dout, s);
+    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s);
     check_launch("slot_reduce");
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
 }

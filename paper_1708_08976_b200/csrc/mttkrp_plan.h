@@ -17,6 +17,12 @@
 //   kKMajorJK rows i, contraction over (j, l) with B = KL(l, :) * KR(j, :)
 //             built per stage (KR materialised by a prologue kernel).
 //             = one_step on interior modes (reference mttkrp.cpp:165-242).
+// swap = 1 runs the paper's 2-step on a boundary mode, where the reference
+// has none: mode 0 as kMMajor on the view (L' = I_0, I' = I_1..I_s, R' =
+// the rest), output index l (rows of X stay contiguous), scale KRP over i';
+// the last mode as kKMajorJ on (L' = I_0..I_{s-1}, I' = I_s..I_{N-2}, R' =
+// I_{N-1}), output index j, scale KRP over i'. Small boundary extents then
+// no longer set the tile height.
 // Work is split stream-K style: the (tile, stage) sequence is cut into
 // equal contiguous ranges, one per CTA; each tile segment a CTA finishes
 // writes one BM-row slot block to the workspace, and a deterministic CSR
@@ -59,6 +65,7 @@ struct TcPlan {
     long long n_lc;           // kKMajorJK: l-chunks of BK * G per j
     long long total_stages;   // n_ti * n_tj * stages_per_tile
     long long kext;           // extent of the B generator index (R for M-major, L for K-major)
+    int swap;                 // epilogue keeps the other row index (boundary-mode 2-step, see below)
     int max_seg;              // workspace slot blocks per CTA
     int debug;                // experiment switches (0 in production)
     KrpGen bgen;              // B operand rows (index j for M-major, l for K-major)

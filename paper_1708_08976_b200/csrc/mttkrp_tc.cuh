@@ -562,7 +562,61 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         const int C = p.C;
         double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * Cfg::BM + RW * w) * C;
         for (int c = lane; c < C; c += 32) {
-            if (!KMAJ) {
+            if (!KMAJ && p.swap) {
+                // boundary 2-step, mode 0: output row l = m % L, scale KRP(i = m / L)
+                const long long mrows = p.L * p.I;
+                const long long mbase = tile * p.TR + RW * lw;
+                if (mbase < mrows) {
+                    const long long ifirst = div_nn(mbase, p.L);
+                    const long long l0 = mbase - ifirst * p.L;
+                    if (p.L >= RW) {  // at most one wrap: two scale rows
+                        const long long rw = p.L - l0;
+                        const double sc0 = krp_scale(p.sgen, ifirst, c);
+                        const double sc1 = (rw < RW && ifirst + 1 < p.I) ? krp_scale(p.sgen, ifirst + 1, c) : 0.0;
+#pragma unroll 4
+                        for (int r = 0; r < RW; ++r)
+                            if (mbase + r < mrows) wsb[r * C + c] = Pw[r * LD + c] * (r < rw ? sc0 : sc1);
+                    } else {
+                        const int nslot = static_cast<int>(p.L);
+                        for (int q = 0; q < nslot && mbase + q < mrows; ++q) {
+                            double sum = 0.0;
+                            for (int r = q; r < RW && mbase + r < mrows; r += nslot)
+                                sum += Pw[r * LD + c] * krp_scale(p.sgen, ifirst + div_nn(l0 + r, p.L), c);
+                            wsb[q * C + c] = sum;
+                        }
+                    }
+                }
+            } else if (KMAJ && p.swap) {
+                // boundary 2-step, last mode: output row j, scale KRP(i)
+                const long long tj = div_nn(tile, p.n_ti);
+                const long long ti = tile - tj * p.n_ti;
+                if (p.BI >= RW) {
+                    const long long j = tj * p.BJ + (RW * lw) / p.BI;
+                    const long long ib = ti * p.BI + (RW * lw) % p.BI;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int r0 = 0; r0 < RW; r0 += EC) {
+                        double sc[EC];
+#pragma unroll
+                        for (int r = 0; r < EC; ++r) sc[r] = ib + r0 + r < p.I ? krp_scale(p.sgen, ib + r0 + r, c) : 0.0;
+#pragma unroll
+                        for (int r = 0; r < EC; ++r) sum += Pw[(r0 + r) * LD + c] * sc[r];
+                    }
+                    if (j < p.R) wsb[c] = sum;
+                } else {
+                    const int njl = RW / p.BI;
+                    const int jl0 = (RW * lw) / p.BI;
+                    for (int q = 0; q < njl; ++q) {
+                        const long long j = tj * p.BJ + jl0 + q;
+                        double sum = 0.0;
+                        for (int il = 0; il < p.BI; ++il) {
+                            const long long i = ti * p.BI + il;
+                            if (i < p.I) sum += Pw[(q * p.BI + il) * LD + c] * krp_scale(p.sgen, i, c);
+                        }
+                        if (j < p.R) wsb[q * C + c] = sum;
+                    }
+                }
+            } else if (!KMAJ) {
                 const long long mrows = p.L * p.I;
                 const long long mbase = tile * p.TR + RW * lw;
                 if (p.L == 1) {

@@ -26,3 +26,25 @@ def test_forced_tile_shape(rb, g):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+
+
+def test_boundary_two_step_views():
+    """Boundary modes with short extents take the swapped 2-step view (plan log
+    'swap 1'); results stay within tolerance on every mode."""
+    env = dict(os.environ, DMTK_GPU_PLAN_LOG="1")
+    shapes = ["40x40x12x8:20", "100x10x30x8:25", "8x60x50:16", "64x4x4x64:32"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+    assert " swap 1 " in r.stderr
+
+
+@pytest.mark.parametrize("rb", [2, 3, 4])
+def test_boundary_two_step_forced_shapes(rb):
+    env = dict(os.environ, DMTK_GPU_FORCE_RB=str(rb))
+    shapes = ["40x40x12x8:20", "100x10x30x8:25", "8x60x50:16", "64x4x4x64:3", "6x10x4x2x2x4:17"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
