@@ -1317,15 +1317,10 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         // from the cached Grams, solve, normalise, refresh this mode's Gram
         auto mode_step = [&](int n) {
             mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
-            launch_hadamard_grams(grams, N, C, n, H, s);
-            check_launch("hadamard_grams");
-            launch_solve_psd(H, C, M.p, t->dims[n], Um[n], solve_scr, ctx.flag, s);
-            count_launch(4);
-            ck(cudaGetLastError(), "solve_psd");
-            launch_normalize_cols(Um[n], t->dims[n], C, lam, s);
-            check_launch("normalize");
-            launch_gram(Um[n], t->dims[n], C, grams + static_cast<long long>(n) * C * C, s);
-            check_launch("gram");
+            const int nl = launch_als_update(grams, N, C, n, H, M.p, t->dims[n], Um[n], lam,
+                                             grams + static_cast<long long>(n) * C * C, solve_scr, ctx.flag, s);
+            count_launch(nl - 1);
+            check_launch("als_update");
         };
         // H and M still hold the last mode's values (cp_als.cpp:149-155)
         auto fit_step = [&]() {

@@ -12,6 +12,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace dmtkg {
 
 // ---------------------------------------------------------------- KRP
@@ -72,15 +74,31 @@ __global__ void mttkrp_generic_kernel(const double* __restrict__ X, long long L,
 
 // ------------------------------------------------------------ CSR reduce
 // out(i, c) = sum_{e in [rowptr[i], rowptr[i+1])} ws(slot[e], c), fixed order.
-__global__ void slot_reduce_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
-                                   const long long* __restrict__ slots, long long rows, int C, double* __restrict__ out) {
-    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= rows * C) return;
-    const long long i = e / C;
-    const int c = static_cast<int>(e - i * C);
+// One CTA per output row: thread (p, c) sums slots k = p, p + P, ... of the
+// row's CSR range for column c (coalesced over c), then the P partials are
+// added in a fixed order: deterministic, and the row's slots are read by
+// P independent load streams instead of one dependent chain.
+constexpr int kReduceThreads = 256;
+__global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const double* __restrict__ ws,
+                                                                     const long long* __restrict__ rowptr,
+                                                                     const long long* __restrict__ slots, int C,
+                                                                     double* __restrict__ out) {
+    __shared__ double part[kReduceThreads];
+    const long long i = blockIdx.x;
+    const int P = kReduceThreads / C;
+    const int p = threadIdx.x / C;
+    const int c = threadIdx.x - p * C;
+    const long long k0 = rowptr[i], k1 = rowptr[i + 1];
     double s = 0.0;
-    for (long long k = rowptr[i]; k < rowptr[i + 1]; ++k) s += ws[slots[k] * C + c];
-    out[e] = s;
+    if (p < P)
+        for (long long k = k0 + p; k < k1; k += P) s += ws[slots[k] * C + c];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < C) {
+        double t = 0.0;
+        for (int q = 0; q < P; ++q) t += part[q * C + threadIdx.x];
+        out[i * C + threadIdx.x] = t;
+    }
 }
 
 // ----------------------------------------------------------- baseline reorder
@@ -129,59 +147,83 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // Cholesky with pivot floor 1e-12 * trace (linalg.cpp:254-276), one CTA.
 // Writes L (row-major, lower) and flag[0] = 1 on success, 0 on failure.
 __global__ void cholesky_kernel(const double* __restrict__ H, int n, double* __restrict__ Lm, int* __restrict__ flag) {
+    // one warp; H and L staged in shared memory. Same operation order as the
+    // reference (linalg.cpp:250-279): d = H_jj - sum_k L_jk^2 ascending in k,
+    // then column j below the diagonal.
     __shared__ double sL[64 * 64];
-    __shared__ double s_root;
-    __shared__ int s_ok;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < n * n; e += blockDim.x) sL[e] = 0.0;
-    if (tid == 0) s_ok = 1;
+    __shared__ double sD[64];  // diagonal of H
+    const int lane = threadIdx.x;
+    for (int e = lane; e < n * n; e += 32) sL[e] = 0.0;
+    for (int k = lane; k < n; k += 32) sD[k] = H[k * n + k];
+    __syncwarp();
     double tr = 0.0;
-    for (int k = 0; k < n; ++k) tr += H[k * n + k];
+    for (int k = 0; k < n; ++k) tr += sD[k];
     const double tol = 1e-12 * tr;
-    __syncthreads();
+    int ok = 1;
     for (int j = 0; j < n; ++j) {
-        if (tid == 0) {
-            double d = H[j * n + j];
-            for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
-            if (d <= tol) {
-                s_ok = 0;
-            } else {
-                s_root = sqrt(d);
-                sL[j * n + j] = s_root;
-            }
+        double d = sD[j];
+        for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
+        if (d <= tol) {  // every lane computes the same d: uniform exit
+            ok = 0;
+            break;
         }
-        __syncthreads();
-        if (!s_ok) break;
-        for (int i = j + 1 + tid; i < n; i += blockDim.x) {
-            double s = H[i * n + j];
-            for (int k = 0; k < j; ++k) s -= sL[i * n + k] * sL[j * n + k];
-            sL[i * n + j] = s / s_root;
+        const double root = sqrt(d);
+        if (lane == 0) sL[j * n + j] = root;
+        for (int i = j + 1 + lane; i < n; i += 32) {
+            double t = __ldg(H + i * n + j);
+            for (int k = 0; k < j; ++k) t -= sL[i * n + k] * sL[j * n + k];
+            sL[i * n + j] = t / root;
         }
-        __syncthreads();
+        __syncwarp();
     }
-    for (int e = tid; e < n * n; e += blockDim.x) Lm[e] = sL[e];
-    if (tid == 0) flag[0] = s_ok;
+    for (int e = lane; e < n * n; e += 32) Lm[e] = sL[e];
+    if (lane == 0) flag[0] = ok;
 }
 
-// Row-wise forward then back substitution (linalg.cpp:340-354).
-__global__ void chol_solve_rows_kernel(const double* __restrict__ Lm, int n, const double* __restrict__ M, long long rows,
-                                       double* __restrict__ U, const int* __restrict__ flag) {
+// Forward then back substitution of one row (linalg.cpp:340-354): w = L^-1 m,
+// u = L^-T w, with the row in registers (NP >= n) and L in shared memory.
+template <int NP>
+__device__ __forceinline__ void solve_row(const double* __restrict__ sL, int n, const double* __restrict__ mrow,
+                                          double* __restrict__ urow) {
+    double w[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) w[j] = j < n ? mrow[j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        if (j < n) {
+            double t = w[j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) t -= sL[j * n + k] * w[k];
+            w[j] = t / sL[j * n + j];
+        }
+    }
+#pragma unroll
+    for (int j = NP - 1; j >= 0; --j) {
+        if (j < n) {
+            double t = w[j];
+#pragma unroll
+            for (int k = j + 1; k < NP; ++k)
+                if (k < n) t -= sL[k * n + j] * w[k];
+            w[j] = t / sL[j * n + j];  // w[k > j] already hold u[k]
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+        if (j < n) urow[j] = w[j];
+}
+
+// Row-wise substitution kernel, one row per thread (solve_row).
+template <int NP>
+__global__ void __launch_bounds__(64) chol_solve_rows_kernel(const double* __restrict__ Lm, int n,
+                                                             const double* __restrict__ M, long long rows,
+                                                             double* __restrict__ U, const int* __restrict__ flag) {
     if (!flag[0]) return;
+    __shared__ double sL[NP * NP];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sL[e] = Lm[e];
+    __syncthreads();
     const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    double w[64];
-    const double* mrow = M + r * n;
-    double* urow = U + r * n;
-    for (int j = 0; j < n; ++j) {
-        double s = mrow[j];
-        for (int k = 0; k < j; ++k) s -= Lm[j * n + k] * w[k];
-        w[j] = s / Lm[j * n + j];
-    }
-    for (int j = n - 1; j >= 0; --j) {
-        double s = w[j];
-        for (int k = j + 1; k < n; ++k) s -= Lm[k * n + j] * urow[k];
-        urow[j] = s / Lm[j * n + j];
-    }
+    solve_row<NP>(sL, n, M + r * n, U + r * n);
 }
 
 // Cyclic Jacobi pseudoinverse fallback (linalg.cpp:281-326, 358-386), one
@@ -386,7 +428,9 @@ __global__ void sumsq_final_kernel(const double* __restrict__ part, int n, doubl
 // G = U^T U, one warp per upper-triangle entry: lane-strided row partial sums
 // then a fixed xor-tree, mirrored to the lower triangle (symmetric to the bit,
 // like linalg.cpp:210-226; deterministic run to run).
-__global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ G) {
+__global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ G,
+                                 const int* __restrict__ only_if_failed) {
+    if (only_if_failed && only_if_failed[0]) return;
     int e = blockIdx.x, c1 = 0;
     while (e >= C - c1) {  // blockIdx -> (c1, c2 >= c1)
         e -= C - c1;
@@ -416,7 +460,9 @@ __global__ void hadamard_grams_kernel(const double* __restrict__ grams, int nmod
 
 // Column 2-norms into lambda and column scaling (cp_als.cpp:101-118); one
 // CTA per column, fixed-order tree reduction.
-__global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda) {
+__global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda,
+                                      const int* __restrict__ only_if_failed) {
+    if (only_if_failed && only_if_failed[0]) return;
     __shared__ double red[256];
     __shared__ double s_norm;
     const int c = blockIdx.x;
@@ -449,25 +495,46 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
                                   const double* __restrict__ lambda, const double* __restrict__ Hlast,
                                   const double* __restrict__ Glast, const double* __restrict__ normx,
                                   double* __restrict__ out) {
+    // <X, Y> from the last mode's MTTKRP and ||Y||^2 from the Grams, both as
+    // fixed-order block reductions (deterministic)
     __shared__ double red[256];
+    __shared__ double red2[256];
+    __shared__ double slam[64];
+    if (threadIdx.x < C) slam[threadIdx.x] = lambda[threadIdx.x];
+    __syncthreads();
     double inner = 0.0;
-    for (long long e = threadIdx.x; e < rows * C; e += blockDim.x) {
-        const int c = static_cast<int>(e % C);
-        inner += Mlast[e] * lambda[c] * U[e];
+    const long long n = rows * C;
+    for (long long r = threadIdx.x / C, c = threadIdx.x % C; r < rows;) {
+        const long long e = r * C + c;
+        inner += Mlast[e] * slam[c] * U[e];
+        c += blockDim.x % C;
+        r += blockDim.x / C;
+        if (c >= C) {
+            c -= C;
+            ++r;
+        }
+    }
+    (void)n;
+    double ny = 0.0;
+    for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+        const int c1 = e / C, c2 = e - (e / C) * C;
+        ny += slam[c1] * slam[c2] * Hlast[e] * Glast[e];
     }
     red[threadIdx.x] = inner;
+    red2[threadIdx.x] = ny;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        if (threadIdx.x < w) {
+            red[threadIdx.x] += red[threadIdx.x + w];
+            red2[threadIdx.x] += red2[threadIdx.x + w];
+        }
         __syncthreads();
     }
     if (threadIdx.x == 0) {
         const double in = red[0];
-        double ny = 0.0;
-        for (int c1 = 0; c1 < C; ++c1)
-            for (int c2 = 0; c2 < C; ++c2) ny += lambda[c1] * lambda[c2] * Hlast[c1 * C + c2] * Glast[c1 * C + c2];
+        const double nyv = red2[0];
         const double nx = normx[0];
-        double res2 = nx * nx - 2.0 * in + ny;
+        double res2 = nx * nx - 2.0 * in + nyv;
         if (res2 < 0.0) res2 = 0.0;
         const double ar = sqrt(res2);
         out[2] = ar;
@@ -479,6 +546,142 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
             out[0] = out[1] = out[3] = 0.0;
         }
     }
+}
+
+// One CP-ALS factor update in a single CTA (small factors: rows * C <= 64K):
+// H = Hadamard of the cached Grams but `skip` (linalg.cpp:228-248), Cholesky
+// (linalg.cpp:250-279), row-wise substitution U = M H^-1 (linalg.cpp:340-354),
+// column 2-norm normalisation into lambda (cp_als.cpp:101-118) and the
+// refreshed Gram of U. Replaces six dependent launches on the ALS critical
+// path. On a failed Cholesky it only writes H and flag = 0; the Jacobi
+// fallback kernels (guarded by the flag) then finish the update.
+// Dynamic shared memory: 2 * C * C + 1024 doubles. 512 threads (256 above
+// rank 32: the row lives in registers).
+template <int NP>
+__global__ void __launch_bounds__(NP <= 32 ? 512 : 256) als_update_kernel(const double* __restrict__ grams, int nmodes, int C, int skip,
+                                                          double* __restrict__ Hout, const double* __restrict__ M,
+                                                          long long rows, double* __restrict__ U,
+                                                          double* __restrict__ lambda, double* __restrict__ Gn,
+                                                          int* __restrict__ flag) {
+    extern __shared__ double sm[];
+    double* sH = sm;
+    double* sL = sm + C * C;
+    double* red = sm + 2 * C * C;  // 1024
+    __shared__ int s_ok;
+    __shared__ double s_inv[64];
+    const int tid = threadIdx.x;
+    const int n = C;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        double h = 1.0;
+        for (int k = 0; k < nmodes; ++k)
+            if (k != skip) h *= grams[static_cast<long long>(k) * n * n + e];
+        sH[e] = h;
+        Hout[e] = h;
+        sL[e] = 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {  // Cholesky, one warp, reference operation order
+        const int lane = tid;
+        double tr = 0.0;
+        for (int k = 0; k < n; ++k) tr += sH[k * n + k];
+        const double tol = 1e-12 * tr;
+        int ok = 1;
+        for (int j = 0; j < n; ++j) {
+            double d = sH[j * n + j];
+            for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
+            if (d <= tol) {
+                ok = 0;
+                break;
+            }
+            const double root = sqrt(d);
+            if (lane == 0) sL[j * n + j] = root;
+            for (int i = j + 1 + lane; i < n; i += 32) {
+                double t = sH[i * n + j];
+                for (int k = 0; k < j; ++k) t -= sL[i * n + k] * sL[j * n + k];
+                sL[i * n + j] = t / root;
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (tid == 0) flag[0] = 0;
+        return;
+    }
+    // substitution, one row per thread, row in registers
+#pragma unroll 1
+    for (int r = tid; r < static_cast<int>(rows); r += blockDim.x) solve_row<NP>(sL, n, M + r * n, U + r * n);
+    __syncthreads();
+    // column norms: thread (p, c) over rows p, p + P, ...; partials added in order
+    const int P = blockDim.x / n;
+    {
+        const int p = tid / n, c = tid - (tid / n) * n;
+        double sq = 0.0;
+        if (p < P)
+            for (long long r = p; r < rows; r += P) {
+                const double v = U[r * n + c];
+                sq = fma(v, v, sq);
+            }
+        red[tid] = sq;
+    }
+    __syncthreads();
+    if (tid < n) {
+        double t = 0.0;
+        for (int q = 0; q < P; ++q) t += red[q * n + tid];
+        const double nrm = sqrt(t);
+        lambda[tid] = nrm;
+        s_inv[tid] = nrm > 0.0 ? 1.0 / nrm : 1.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < static_cast<int>(rows) * n; e += blockDim.x) U[e] *= s_inv[e % n];
+    __syncthreads();
+    // Gram of the normalised factor: entry (c1 <= c2) x part
+    const int ne = n * (n + 1) / 2;
+    const int parts = blockDim.x / ne > 0 ? blockDim.x / ne : 1;
+    for (int base = 0; base < ne * parts; base += blockDim.x) {
+        const int x = base + tid;
+        double g = 0.0;
+        if (x < ne * parts) {
+            const int ent = x % ne, part = x / ne;
+            int c1 = 0, e = ent;
+            while (e >= n - c1) {
+                e -= n - c1;
+                ++c1;
+            }
+            const int c2 = c1 + e;
+            for (long long r = part; r < rows; r += parts) g = fma(U[r * n + c1], U[r * n + c2], g);
+        }
+        __syncthreads();
+        if (x < ne * parts) red[x - base] = g;
+        __syncthreads();
+        // (ne * parts <= blockDim.x whenever parts > 1; otherwise one pass per block of entries)
+        if (parts > 1) {
+            if (tid < ne) {
+                double t = 0.0;
+                for (int q = 0; q < parts; ++q) t += red[q * ne + tid];
+                int c1 = 0, e = tid;
+                while (e >= n - c1) {
+                    e -= n - c1;
+                    ++c1;
+                }
+                const int c2 = c1 + e;
+                Gn[c1 * n + c2] = t;
+                Gn[c2 * n + c1] = t;
+            }
+        } else if (x < ne) {
+            int c1 = 0, e = x;
+            while (e >= n - c1) {
+                e -= n - c1;
+                ++c1;
+            }
+            const int c2 = c1 + e;
+            Gn[c1 * n + c2] = red[tid];
+            Gn[c2 * n + c1] = red[tid];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) flag[0] = 1;
 }
 
 // --------------------------------------------------------- FP64 peak probe
@@ -518,8 +721,8 @@ void launch_mttkrp_generic(const double* X, long long L, long long I, long long 
 
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
                         double* out, cudaStream_t s) {
-    const long long n = rows * C;
-    slot_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, rowptr, slots, rows, C, out);
+    if (rows <= 0) return;
+    slot_reduce_kernel<<<static_cast<unsigned>(rows), kReduceThreads, 0, s>>>(ws, rowptr, slots, C, out);
 }
 
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s) {
@@ -540,9 +743,19 @@ void launch_solve_psd(const double* H, int n, const double* M, long long rows, d
     double* Lm = scratch;            // n*n
     double* V = scratch + 64 * 64;   // n*n
     double* gain = V + 64 * 64;      // n
-    cholesky_kernel<<<1, 128, 0, s>>>(H, n, Lm, flag);
+    cholesky_kernel<<<1, 32, 0, s>>>(H, n, Lm, flag);
+    const unsigned gs = static_cast<unsigned>((rows + 63) / 64);
+    switch ((n + 7) / 8) {
+        case 1: chol_solve_rows_kernel<8><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 2: chol_solve_rows_kernel<16><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 3: chol_solve_rows_kernel<24><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 4: chol_solve_rows_kernel<32><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 5: chol_solve_rows_kernel<40><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 6: chol_solve_rows_kernel<48><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 7: chol_solve_rows_kernel<56><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        default: chol_solve_rows_kernel<64><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+    }
     const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-    chol_solve_rows_kernel<<<gb, 128, 0, s>>>(Lm, n, M, rows, U, flag);
     jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
     jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, n, M, rows, U, flag);
 }
@@ -562,7 +775,7 @@ void launch_tensor_norm(const double* x, long long n, double* part, int nparts, 
 }
 
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s) {
-    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, G);
+    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, G, nullptr);
 }
 
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s) {
@@ -570,7 +783,52 @@ void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, dou
 }
 
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
-    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda);
+    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr);
+}
+
+template <int NP>
+static void launch_als_fused(const double* grams, int nmodes, int C, int skip, double* H, const double* M,
+                             long long rows, double* U, double* lambda, double* Gn, int* flag, cudaStream_t s) {
+    const int smem = (2 * C * C + 1024) * 8;
+    static int opted = 0;
+    if (smem > 48 * 1024 && !opted) {
+        cudaFuncSetAttribute(als_update_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        opted = 1;
+    }
+    als_update_kernel<NP><<<1, NP <= 32 ? 512 : 256, smem, s>>>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn,
+                                                                flag);
+}
+
+int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
+                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s) {
+    static const bool fused = std::getenv("DMTK_GPU_ALS_FUSED") != nullptr;  // experiment: measured slower
+    if (!fused || rows * C > 65536) {
+        launch_hadamard_grams(grams, nmodes, C, skip, H, s);
+        launch_solve_psd(H, C, M, rows, U, scratch, flag, s);
+        launch_normalize_cols(U, rows, C, lambda, s);
+        launch_gram(U, rows, C, Gn, s);
+        return 7;
+    }
+    switch ((C + 7) / 8) {
+        case 1: launch_als_fused<8>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 2: launch_als_fused<16>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 3: launch_als_fused<24>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 4: launch_als_fused<32>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 5: launch_als_fused<40>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 6: launch_als_fused<48>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        case 7: launch_als_fused<56>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+        default: launch_als_fused<64>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
+    }
+    // Cholesky failed (flag 0): Jacobi pseudoinverse, then normalise + Gram;
+    // every one of these exits at once when the fused update succeeded
+    double* V = scratch + 64 * 64;
+    double* gain = V + 64 * 64;
+    jacobi_kernel<<<1, 64, 0, s>>>(H, C, V, gain, flag);
+    const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
+    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, C, M, rows, U, flag);
+    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, flag);
+    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, Gn, flag);
+    return 5;
 }
 
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,

@@ -28,6 +28,10 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s);
+// One ALS factor update (Hadamard of cached Grams, solve, normalise, new
+// Gram); fused into one CTA for small factors. Returns the launch count.
+int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
+                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s);
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s);
 

@@ -1,0 +1,63 @@
+"""Kernel timeline of a CP-ALS run (developer tool): CUPTI via torch.profiler,
+per-iteration kernel busy time vs wall, and the largest idle gaps.
+
+python tools/als_timeline.py [--dims 100,100,1200,80] [--rank 20] [--iters 6]
+"""
+import argparse
+import os
+import sys
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1708_08976_b200 as dg  # noqa: E402
+from tools.perf_als import fmri_tensor  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dims", default="100,100,1200,80")
+    ap.add_argument("--rank", type=int, default=20)
+    ap.add_argument("--iters", type=int, default=6)
+    a = ap.parse_args()
+    dims = tuple(int(d) for d in a.dims.split(","))
+    x = fmri_tensor(dims)
+    t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
+    dg.cp_als(t, dg.AlsConfig(rank=a.rank, max_iters=2, tol=0.0, seed=1))
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        dg.cp_als(t, dg.AlsConfig(rank=a.rank, max_iters=a.iters, tol=0.0, seed=1))
+        torch.cuda.synchronize()
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    ev.sort(key=lambda e: e.time_range.start)
+    t0 = ev[0].time_range.start
+    busy = {}
+    gaps = []
+    prev_end = None
+    for e in ev:
+        s, d = e.time_range.start, e.time_range.end
+        nm = e.name.split("(")[0].replace("void ", "").replace("dmtkg::", "")[:40]
+        busy[nm] = busy.get(nm, 0.0) + (d - s)
+        if prev_end is not None and s > prev_end:
+            gaps.append((s - prev_end, nm, s - t0))
+        prev_end = max(prev_end or 0, d)
+    span = prev_end - t0
+    print(f"span {span:.0f} us, kernels busy {sum(busy.values()):.0f} us, idle {sum(g[0] for g in gaps):.0f} us")
+    for k, v in sorted(busy.items(), key=lambda kv: -kv[1])[:14]:
+        print(f"  {k:40s} {v:9.1f} us")
+    gaps.sort(reverse=True)
+    print("largest gaps (us, next kernel, at):")
+    for g in gaps[:12]:
+        print(f"  {g[0]:8.1f} before {g[1]:40s} at {g[2]:9.1f}")
+    # gap histogram
+    tot = {}
+    for g, nm, _ in gaps:
+        tot[nm] = tot.get(nm, 0.0) + g
+    print("idle before each kernel kind:")
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:10]:
+        print(f"  {k:40s} {v:9.1f} us")
+
+
+if __name__ == "__main__":
+    main()
