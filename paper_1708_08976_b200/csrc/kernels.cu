@@ -226,6 +226,80 @@ __global__ void __launch_bounds__(64) chol_solve_rows_kernel(const double* __res
     solve_row<NP>(sL, n, M + r * n, U + r * n);
 }
 
+// CP-ALS fast solve: Cholesky (same operation order as cholesky_kernel),
+// then H^-1 = L^-T L^-1 explicitly, so that U = M H^-1 is one independent
+// dot product per output element instead of a 2 n^2-deep dependent chain per
+// row. One warp; dynamic shared memory 2 n^2 doubles. Used by the on-device
+// ALS loop (cp_als); dmtk_gpu_solve_psd keeps the reference's substitution.
+__global__ void cholesky_inverse_kernel(const double* __restrict__ H, int n, double* __restrict__ Hinv,
+                                        int* __restrict__ flag) {
+    extern __shared__ double shm[];
+    double* sL = shm;
+    double* sLi = shm + n * n;
+    __shared__ double sD[64];
+    const int lane = threadIdx.x;
+    for (int e = lane; e < n * n; e += 32) {
+        sL[e] = 0.0;
+        sLi[e] = 0.0;
+    }
+    for (int k = lane; k < n; k += 32) sD[k] = H[k * n + k];
+    __syncwarp();
+    double tr = 0.0;
+    for (int k = 0; k < n; ++k) tr += sD[k];
+    const double tol = 1e-12 * tr;
+    for (int j = 0; j < n; ++j) {
+        double d = sD[j];
+        for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
+        if (d <= tol) {
+            if (lane == 0) flag[0] = 0;
+            return;
+        }
+        const double root = sqrt(d);
+        if (lane == 0) sL[j * n + j] = root;
+        for (int i = j + 1 + lane; i < n; i += 32) {
+            double t = __ldg(H + i * n + j);
+            for (int k = 0; k < j; ++k) t -= sL[i * n + k] * sL[j * n + k];
+            sL[i * n + j] = t / root;
+        }
+        __syncwarp();
+    }
+    // column c of L^-1 by forward substitution on e_c
+    for (int c = lane; c < n; c += 32) {
+        sLi[c * n + c] = 1.0 / sL[c * n + c];
+        for (int j = c + 1; j < n; ++j) {
+            double t = 0.0;
+            for (int k = c; k < j; ++k) t -= sL[j * n + k] * sLi[k * n + c];
+            sLi[j * n + c] = t / sL[j * n + j];
+        }
+    }
+    __syncwarp();
+    // H^-1[a][b] = sum_{k >= max(a, b)} Li[k][a] Li[k][b]
+    for (int e = lane; e < n * n; e += 32) {
+        const int a = e / n, b = e - (e / n) * n;
+        double t = 0.0;
+        for (int k = a > b ? a : b; k < n; ++k) t += sLi[k * n + a] * sLi[k * n + b];
+        Hinv[e] = t;
+    }
+    if (lane == 0) flag[0] = 1;
+}
+
+// U = M H^-1, one output element per thread (H^-1 staged in shared memory).
+__global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, const double* __restrict__ M,
+                                     long long rows, double* __restrict__ U, const int* __restrict__ flag) {
+    if (!flag[0]) return;
+    extern __shared__ double sHi[];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sHi[e] = Hinv[e];
+    __syncthreads();
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= rows * n) return;
+    const long long r = e / n;
+    const int c = static_cast<int>(e - r * n);
+    const double* mrow = M + r * n;
+    double t = 0.0;
+    for (int k = 0; k < n; ++k) t = fma(mrow[k], sHi[k * n + c], t);
+    U[e] = t;
+}
+
 // Cyclic Jacobi pseudoinverse fallback (linalg.cpp:281-326, 358-386), one
 // CTA; only runs when the Cholesky flag is 0. Produces V and gain.
 __global__ void jacobi_kernel(const double* __restrict__ H, int n, double* __restrict__ Vout, double* __restrict__ gain,
@@ -548,142 +622,6 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
     }
 }
 
-// One CP-ALS factor update in a single CTA (small factors: rows * C <= 64K):
-// H = Hadamard of the cached Grams but `skip` (linalg.cpp:228-248), Cholesky
-// (linalg.cpp:250-279), row-wise substitution U = M H^-1 (linalg.cpp:340-354),
-// column 2-norm normalisation into lambda (cp_als.cpp:101-118) and the
-// refreshed Gram of U. Replaces six dependent launches on the ALS critical
-// path. On a failed Cholesky it only writes H and flag = 0; the Jacobi
-// fallback kernels (guarded by the flag) then finish the update.
-// Dynamic shared memory: 2 * C * C + 1024 doubles. 512 threads (256 above
-// rank 32: the row lives in registers).
-template <int NP>
-__global__ void __launch_bounds__(NP <= 32 ? 512 : 256) als_update_kernel(const double* __restrict__ grams, int nmodes, int C, int skip,
-                                                          double* __restrict__ Hout, const double* __restrict__ M,
-                                                          long long rows, double* __restrict__ U,
-                                                          double* __restrict__ lambda, double* __restrict__ Gn,
-                                                          int* __restrict__ flag) {
-    extern __shared__ double sm[];
-    double* sH = sm;
-    double* sL = sm + C * C;
-    double* red = sm + 2 * C * C;  // 1024
-    __shared__ int s_ok;
-    __shared__ double s_inv[64];
-    const int tid = threadIdx.x;
-    const int n = C;
-    for (int e = tid; e < n * n; e += blockDim.x) {
-        double h = 1.0;
-        for (int k = 0; k < nmodes; ++k)
-            if (k != skip) h *= grams[static_cast<long long>(k) * n * n + e];
-        sH[e] = h;
-        Hout[e] = h;
-        sL[e] = 0.0;
-    }
-    __syncthreads();
-    if (tid < 32) {  // Cholesky, one warp, reference operation order
-        const int lane = tid;
-        double tr = 0.0;
-        for (int k = 0; k < n; ++k) tr += sH[k * n + k];
-        const double tol = 1e-12 * tr;
-        int ok = 1;
-        for (int j = 0; j < n; ++j) {
-            double d = sH[j * n + j];
-            for (int k = 0; k < j; ++k) d -= sL[j * n + k] * sL[j * n + k];
-            if (d <= tol) {
-                ok = 0;
-                break;
-            }
-            const double root = sqrt(d);
-            if (lane == 0) sL[j * n + j] = root;
-            for (int i = j + 1 + lane; i < n; i += 32) {
-                double t = sH[i * n + j];
-                for (int k = 0; k < j; ++k) t -= sL[i * n + k] * sL[j * n + k];
-                sL[i * n + j] = t / root;
-            }
-            __syncwarp();
-        }
-        if (lane == 0) s_ok = ok;
-    }
-    __syncthreads();
-    if (!s_ok) {
-        if (tid == 0) flag[0] = 0;
-        return;
-    }
-    // substitution, one row per thread, row in registers
-#pragma unroll 1
-    for (int r = tid; r < static_cast<int>(rows); r += blockDim.x) solve_row<NP>(sL, n, M + r * n, U + r * n);
-    __syncthreads();
-    // column norms: thread (p, c) over rows p, p + P, ...; partials added in order
-    const int P = blockDim.x / n;
-    {
-        const int p = tid / n, c = tid - (tid / n) * n;
-        double sq = 0.0;
-        if (p < P)
-            for (long long r = p; r < rows; r += P) {
-                const double v = U[r * n + c];
-                sq = fma(v, v, sq);
-            }
-        red[tid] = sq;
-    }
-    __syncthreads();
-    if (tid < n) {
-        double t = 0.0;
-        for (int q = 0; q < P; ++q) t += red[q * n + tid];
-        const double nrm = sqrt(t);
-        lambda[tid] = nrm;
-        s_inv[tid] = nrm > 0.0 ? 1.0 / nrm : 1.0;
-    }
-    __syncthreads();
-    for (int e = tid; e < static_cast<int>(rows) * n; e += blockDim.x) U[e] *= s_inv[e % n];
-    __syncthreads();
-    // Gram of the normalised factor: entry (c1 <= c2) x part
-    const int ne = n * (n + 1) / 2;
-    const int parts = blockDim.x / ne > 0 ? blockDim.x / ne : 1;
-    for (int base = 0; base < ne * parts; base += blockDim.x) {
-        const int x = base + tid;
-        double g = 0.0;
-        if (x < ne * parts) {
-            const int ent = x % ne, part = x / ne;
-            int c1 = 0, e = ent;
-            while (e >= n - c1) {
-                e -= n - c1;
-                ++c1;
-            }
-            const int c2 = c1 + e;
-            for (long long r = part; r < rows; r += parts) g = fma(U[r * n + c1], U[r * n + c2], g);
-        }
-        __syncthreads();
-        if (x < ne * parts) red[x - base] = g;
-        __syncthreads();
-        // (ne * parts <= blockDim.x whenever parts > 1; otherwise one pass per block of entries)
-        if (parts > 1) {
-            if (tid < ne) {
-                double t = 0.0;
-                for (int q = 0; q < parts; ++q) t += red[q * ne + tid];
-                int c1 = 0, e = tid;
-                while (e >= n - c1) {
-                    e -= n - c1;
-                    ++c1;
-                }
-                const int c2 = c1 + e;
-                Gn[c1 * n + c2] = t;
-                Gn[c2 * n + c1] = t;
-            }
-        } else if (x < ne) {
-            int c1 = 0, e = x;
-            while (e >= n - c1) {
-                e -= n - c1;
-                ++c1;
-            }
-            const int c2 = c1 + e;
-            Gn[c1 * n + c2] = red[tid];
-            Gn[c2 * n + c1] = red[tid];
-        }
-        __syncthreads();
-    }
-    if (tid == 0) flag[0] = 1;
-}
-
 // --------------------------------------------------------- FP64 peak probe
 __global__ void dmma_peak_kernel(double* out, int iters) {
     double acc[8][2];
@@ -786,49 +724,38 @@ void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cud
     normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr);
 }
 
-template <int NP>
-static void launch_als_fused(const double* grams, int nmodes, int C, int skip, double* H, const double* M,
-                             long long rows, double* U, double* lambda, double* Gn, int* flag, cudaStream_t s) {
-    const int smem = (2 * C * C + 1024) * 8;
+void launch_solve_psd_inverse(const double* H, int n, const double* M, long long rows, double* U, double* scratch,
+                              int* flag, cudaStream_t s) {
+    double* Hinv = scratch;
+    double* V = scratch + 64 * 64;
+    double* gain = V + 64 * 64;
+    const int sm2 = 2 * n * n * 8;
     static int opted = 0;
-    if (smem > 48 * 1024 && !opted) {
-        cudaFuncSetAttribute(als_update_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (!opted) {
+        cudaFuncSetAttribute(cholesky_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
         opted = 1;
     }
-    als_update_kernel<NP><<<1, NP <= 32 ? 512 : 256, smem, s>>>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn,
-                                                                flag);
+    cholesky_inverse_kernel<<<1, 32, sm2, s>>>(H, n, Hinv, flag);
+    const long long tot = rows * n;
+    apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, n * n * 8, s>>>(Hinv, n, M, rows, U, flag);
+    jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
+    const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
+    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, n, M, rows, U, flag);
 }
 
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
                       double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s) {
-    static const bool fused = std::getenv("DMTK_GPU_ALS_FUSED") != nullptr;  // experiment: measured slower
-    if (!fused || rows * C > 65536) {
-        launch_hadamard_grams(grams, nmodes, C, skip, H, s);
+    // (a single-CTA fusion of these steps was measured slower: one CTA's
+    // latency chains cost more than the launches it saves)
+    static const bool exact = std::getenv("DMTK_GPU_ALS_EXACT_SOLVE") != nullptr;
+    launch_hadamard_grams(grams, nmodes, C, skip, H, s);
+    if (exact)
         launch_solve_psd(H, C, M, rows, U, scratch, flag, s);
-        launch_normalize_cols(U, rows, C, lambda, s);
-        launch_gram(U, rows, C, Gn, s);
-        return 7;
-    }
-    switch ((C + 7) / 8) {
-        case 1: launch_als_fused<8>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 2: launch_als_fused<16>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 3: launch_als_fused<24>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 4: launch_als_fused<32>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 5: launch_als_fused<40>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 6: launch_als_fused<48>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        case 7: launch_als_fused<56>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-        default: launch_als_fused<64>(grams, nmodes, C, skip, H, M, rows, U, lambda, Gn, flag, s); break;
-    }
-    // Cholesky failed (flag 0): Jacobi pseudoinverse, then normalise + Gram;
-    // every one of these exits at once when the fused update succeeded
-    double* V = scratch + 64 * 64;
-    double* gain = V + 64 * 64;
-    jacobi_kernel<<<1, 64, 0, s>>>(H, C, V, gain, flag);
-    const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, C, M, rows, U, flag);
-    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, flag);
-    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, Gn, flag);
-    return 5;
+    else
+        launch_solve_psd_inverse(H, C, M, rows, U, scratch, flag, s);
+    launch_normalize_cols(U, rows, C, lambda, s);
+    launch_gram(U, rows, C, Gn, s);
+    return 7;
 }
 
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,

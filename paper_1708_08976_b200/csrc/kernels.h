@@ -17,6 +17,10 @@ void launch_matricize(const double* X, long long L, long long I, long long R, do
 void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);
 // scratch: >= 2*64*64 + 64 doubles; flag: 1 int
+// Same contract through H^-1 = L^-T L^-1 and one dot product per output
+// element (the ALS loop's fast path; rounding differs from the substitution).
+void launch_solve_psd_inverse(const double* H, int n, const double* M, long long rows, double* U, double* scratch,
+                              int* flag, cudaStream_t s);
 void launch_solve_psd(const double* H, int n, const double* M, long long rows, double* U, double* scratch, int* flag,
                       cudaStream_t s);
 void launch_normalize(double* U, long long rows, int C, double* lambda, cudaStream_t s);
@@ -28,8 +32,8 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s);
-// One ALS factor update (Hadamard of cached Grams, solve, normalise, new
-// Gram); fused into one CTA for small factors. Returns the launch count.
+// One ALS factor update (Hadamard of cached Grams, solve through H^-1,
+// normalise, new Gram). Returns the launch count.
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
                       double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s);
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
