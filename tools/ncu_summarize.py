@@ -6,7 +6,8 @@ python tools/ncu_summarize.py launches <launch-list.csv> <out_prefix>
     total, mean, share of the captured GPU time).
 python tools/ncu_summarize.py full <out.json> <rep.ncu-rep>...
     `ncu --set full` reports -> one JSON record per profiled kernel with the
-    numbers DESIGN.md and bench.py's roofline.traffic cite; also rewrites
+    numbers DESIGN.md and bench.py's roofline.traffic cite; when <out.json>
+    names the bench workload (1000c25) it also rewrites
     profiles/ncu_traffic.json (mean DRAM read+write bytes per launch).
 """
 import csv
@@ -78,7 +79,7 @@ def full(out, reps):
             val, unit = r[k].split()
             b += float(val) * SCALE[unit]
         tr.append(b)
-    if tr:
+    if tr and "1000c25" in os.path.basename(out):
         path = os.path.join(os.path.dirname(out), "ncu_traffic.json")
         json.dump({"1000c25": int(sum(tr) / len(tr)),
                    "_note": "mean dram read+write bytes per mttkrp_tc launch over " + ", ".join(
