@@ -377,6 +377,31 @@ def main():
                "data": "synthetic symmetric slices, unit diagonal, tanh(N(0, 0.3^2)) off-diagonal (torch, seeded)"}
         del xf, tf
 
+    # ----------------- BASELINE config 0: the 3-matrix Khatri-Rao product
+    krp = None
+    if world == 1 and not args.no_als:
+        g = torch.Generator(device=dev).manual_seed(5)
+        kin = [torch.rand((200, 16), dtype=torch.float64, device=dev, generator=g) for _ in range(3)]
+        kout = torch.empty((200 ** 3, 16), dtype=torch.float64, device=dev)
+        kscr = torch.empty((2 * 200 * 200, 16), dtype=torch.float64, device=dev)
+        kcall = lambda: dg.krp_device([a.data_ptr() for a in kin], [200, 200, 200], 16, kout.data_ptr(),
+                                      kscr.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        kcall()
+        torch.cuda.synchronize()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        for _ in range(10):
+            kcall()
+        k1.record()
+        torch.cuda.synchronize()
+        kms = k0.elapsed_time(k1) / 10
+        kgb = 8.0 * 200 ** 3 * 16 / 1e9
+        krp = {"workload": "KRP of three 200x16 factors -> 8e6 x 16 (1.024 GB written; BASELINE config 0)",
+               "ms": round(kms, 4), "GBs_written": round(kgb / (kms * 1e-3), 1),
+               "frac_roofline": round(kgb / hbm_peak / (kms * 1e-3), 3),
+               "note": "bitwise equal to the reference KRP; bytes = output written (SURVEY 8d)"}
+        del kin, kout, kscr
+
     if rank_id == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -399,6 +424,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "cp_als": als,
+            "krp": krp,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

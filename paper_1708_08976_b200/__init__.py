@@ -30,6 +30,7 @@ from .api import (  # noqa: F401
     fp64_peak_tflops_sustained,
     gram_hadamard,
     krp,
+    krp_device,
     krp_naive,
     krp_small,
     launch_count,

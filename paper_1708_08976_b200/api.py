@@ -267,6 +267,18 @@ def krp_small(inputs: Sequence[np.ndarray], stats: Optional[KrpStats] = None, de
     return _krp(inputs, 0, stats, device)
 
 
+def krp_device(device_input_ptrs: Sequence[int], rows: Sequence[int], cols: int, out_ptr: int,
+               scratch_ptr: int = 0, stream: int = 0) -> None:
+    """Device-resident KRP (dmtk_gpu_krp_device): inputs and output already in
+    HBM (row-major), enqueued on `stream` without a host sync. scratch holds
+    prod(rows[:-1]) * cols doubles when len(rows) > 2."""
+    z = len(device_input_ptrs)
+    arr = (C.c_void_p * max(z, 1))(*device_input_ptrs)
+    r = np.asarray(rows, dtype=np.int64)
+    _check(lib.dmtk_gpu_krp_device(z, arr, r.ctypes.data_as(_lib.i64p), cols, C.c_void_p(out_ptr),
+                                   C.c_void_p(scratch_ptr or None), C.c_void_p(stream or None)))
+
+
 def tensor_norm(x: DenseTensor) -> float:
     """dmtk::tensor_norm (cp_als.hpp:68)."""
     out = np.zeros(1)

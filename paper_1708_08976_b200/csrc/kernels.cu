@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace dmtkg {
@@ -21,32 +22,43 @@ namespace dmtkg {
 // level by level this is the cached-partial generator of krp.cpp:53-88 (each
 // level's rows are the partial products P(z) of krp.hpp:27-31) with the same
 // left-to-right association, hence bitwise equal to oracle::krp_kron.
-__global__ void krp_level_kernel(const double* __restrict__ P, const double* __restrict__ U, double* __restrict__ out,
-                                 long long rows_out, long long J, int C) {
-    const long long total = rows_out * C;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    if ((C & 1) == 0) {
-        const long long half = total >> 1;
-        for (long long e2 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e2 < half; e2 += stride) {
-            const long long e = e2 << 1;
-            const long long row = e / C;
-            const int c = static_cast<int>(e - row * C);
-            const long long q = row / J;
-            const long long r = row - q * J;
-            const double2 a = *reinterpret_cast<const double2*>(P + q * C + c);
-            const double2 b = *reinterpret_cast<const double2*>(U + r * C + c);
-            double2 o;
-            o.x = a.x * b.x;
-            o.y = a.y * b.y;
-            __stcs(reinterpret_cast<double2*>(out + e), o);
+constexpr long long kKrpChunk = 4096;  // doubles per work unit (32 KB of output)
+__global__ void __launch_bounds__(256) krp_level_kernel(const double* __restrict__ P, const double* __restrict__ U,
+                                                        double* __restrict__ out, long long Q, int J, int C) {
+    // Output rows q*J .. q*J + J - 1 form one contiguous J*C block equal to U
+    // with column c scaled by P(q, c). Work units are 32 KB chunks of those
+    // blocks (balanced over the grid whatever Q is); inside a unit every
+    // thread advances its column incrementally, so there is no per-entry
+    // index division. One multiply per entry: bitwise the reference's
+    // P(z-1) (.) U_z (krp.hpp:27-31).
+    const long long JC = static_cast<long long>(J) * C;
+    const long long nch = (JC + kKrpChunk - 1) / kKrpChunk;
+    const long long units = Q * nch;
+    const int step = (2 * blockDim.x) % C;  // column advance per 2*blockDim entries
+    // 16-byte vectors when U, out and every block start are 16-byte aligned
+    const bool vec = (JC & 1) == 0 && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        const long long q = unit / nch;
+        const long long f0 = (unit - q * nch) * kKrpChunk;
+        const long long f1 = f0 + kKrpChunk < JC ? f0 + kKrpChunk : JC;
+        const double* __restrict__ Pq = P + q * C;
+        double* o = out + q * JC;
+        if (vec) {
+            const long long fs = f0 + 2 * threadIdx.x;
+            int c = static_cast<int>(fs % C);
+            for (long long f = fs; f < f1; f += 2 * blockDim.x) {
+                const double2 u = __ldg(reinterpret_cast<const double2*>(U + f));
+                const int c1 = c + 1 == C ? 0 : c + 1;
+                double2 v;
+                v.x = __ldg(Pq + c) * u.x;
+                v.y = __ldg(Pq + c1) * u.y;
+                __stcs(reinterpret_cast<double2*>(o + f), v);
+                c += step;
+                if (c >= C) c -= C;
+            }
+        } else {
+            for (long long f = f0 + threadIdx.x; f < f1; f += blockDim.x) o[f] = __ldg(Pq + f % C) * __ldg(U + f);
         }
-        return;
-    }
-    for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-        const long long row = e / C;
-        const int c = static_cast<int>(e - row * C);
-        const long long q = row / J;
-        out[e] = P[q * C + c] * U[(row - q * J) * C + c];
     }
 }
 
@@ -647,8 +659,11 @@ static inline int blocks_for(long long n, int tpb, int cap = 148 * 32) {
 
 void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
                       cudaStream_t s) {
-    const long long n = rows_out * C;
-    krp_level_kernel<<<blocks_for((n + 1) / 2, 256), 256, 0, s>>>(P, U, out, rows_out, J, C);
+    const long long Q = rows_out / J;
+    const long long units = Q * ((J * C + kKrpChunk - 1) / kKrpChunk);
+    const long long blocks = std::min<long long>(units, 148LL * 8);
+    krp_level_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(P, U, out, Q,
+                                                                                          static_cast<int>(J), C);
 }
 
 void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,

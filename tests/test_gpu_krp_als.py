@@ -166,3 +166,20 @@ def test_tensor_norm(oracle, ref):
     dims = (30, 20, 11)
     x = oracle.gen_tensor(dims, 2)
     assert abs(dg.tensor_norm(dg.DenseTensor(dims, x)) - ref.tensor_norm(x, dims)) <= 1e-13 * ref.tensor_norm(x, dims)
+
+
+@pytest.mark.parametrize("rows,C", [((37, 11, 6), 6), ((200, 200, 9), 16), ((5, 7), 25), ((64, 3, 64, 2), 3)])
+def test_krp_device_bitwise(rows, C):
+    """Device-resident KRP (16-byte vector path on aligned torch buffers) is
+    bitwise the host-API KRP (and hence the reference, test_krp.cpp:69-81)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(11)
+    ins = [torch.rand((r, C), dtype=torch.float64, device="cuda", generator=g) for r in rows]
+    total = int(np.prod(rows))
+    out = torch.empty((total, C), dtype=torch.float64, device="cuda")
+    scr = torch.empty((2 * max(1, int(np.prod(rows[:-1]))), C), dtype=torch.float64, device="cuda")
+    dg.krp_device([t.data_ptr() for t in ins], list(rows), C, out.data_ptr(), scr.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    host = dg.krp([t.cpu().numpy() for t in ins])
+    assert np.array_equal(out.cpu().numpy(), host)

@@ -86,6 +86,13 @@ __global__ void read_kernel(const double2* __restrict__ x, size_t n2, double* ou
   if (s0 + s1 == 12345.678) out[0] = s0;
 }
 
+
+__global__ void write_kernel(double2* __restrict__ x, size_t n2, double v) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride)
+    __stcs(x + i, make_double2(v, v + 1.0));
+}
+
 __global__ void fill_kernel(double* x, size_t n) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     x[i] = (double)(i & 1023) * 1e-3;
@@ -205,6 +212,24 @@ int main() {
       CK(cudaEventElapsedTime(&ms, e0, e1));
       std::printf("read-stream blocks/sm %d tpb %d: %.1f GB/s\n", per_sm, tpb, 5.0 * n * 8 / ms / 1e6);
     }
+  }
+  for (int per_sm : {4, 8, 16}) {
+    const int tpb = 256, grid = sms * per_sm;
+    write_kernel<<<grid, tpb>>>((double2*)x, n / 2, 1.0);
+    CK(cudaEventRecord(e0));
+    for (int r = 0; r < 5; ++r) write_kernel<<<grid, tpb>>>((double2*)x, n / 2, 1.0 + r);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::printf("write-stream blocks/sm %d: %.1f GB/s\n", per_sm, 5.0 * n * 8 / ms / 1e6);
+  }
+  for (int r = 0; r < 2; ++r) {
+    CK(cudaEventRecord(e0));
+    CK(cudaMemsetAsync(x, r, n * 8));
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::printf("cudaMemset: %.1f GB/s\n", n * 8 / ms / 1e6);
   }
   CK(cudaFree(x));
   return 0;
