@@ -369,11 +369,24 @@ def main():
         res = dg.cp_als(tf, dg.AlsConfig(rank=20, max_iters=25, tol=0.0, seed=1))
         wall = time.perf_counter() - t0
         it_ms = sorted(1e3 * r.total_seconds for r in res.trace.iters)
+        # the same run as a dimension tree (two tensor passes per iteration)
+        dg.cp_als(tf, dg.AlsConfig(rank=20, max_iters=2, tol=0.0, seed=1, dimension_tree=True))
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        rt = dg.cp_als(tf, dg.AlsConfig(rank=20, max_iters=25, tol=0.0, seed=1, dimension_tree=True))
+        wall_t = time.perf_counter() - t1
+        it_t = sorted(1e3 * r.total_seconds for r in rt.trace.iters)
         nf = int(np.prod(fd))
         als = {"workload": "fMRI-shaped 100x100x1200x80, rank 20, 25 iterations, tol 0 (BASELINE config 5)",
                "iter_ms_median": round(it_ms[len(it_ms) // 2], 3), "wall_s": round(wall, 4),
                "final_fit": res.trace.iters[-1].fit.fit,
                "roofline_iter_ms": round(4 * 8.0 * nf / (hbm_peak * 1e9) * 1e3, 3),
+               "dimension_tree": {"iter_ms_median": round(it_t[len(it_t) // 2], 3), "wall_s": round(wall_t, 4),
+                                  "final_fit": rt.trace.iters[-1].fit.fit,
+                                  "max_fit_diff_vs_per_mode": float(max(abs(a.fit.fit - b.fit.fit) for a, b in
+                                                                        zip(res.trace.iters, rt.trace.iters))),
+                                  "roofline_iter_ms": round(2 * 8.0 * nf / (hbm_peak * 1e9) * 1e3, 3),
+                                  "note": "same ALS updates, two tensor passes per iteration (SURVEY 8f-2)"},
                "data": "synthetic symmetric slices, unit diagonal, tanh(N(0, 0.3^2)) off-diagonal (torch, seeded)"}
         del xf, tf
 

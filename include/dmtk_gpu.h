@@ -115,7 +115,15 @@ int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t ra
                            int64_t skip, double* h_out);
 int dmtk_gpu_solve_psd(int device, int64_t rank, const double* h, int64_t rows, const double* m, double* u_out);
 
-/* AlsConfig (cp_als.hpp:32-40). */
+/* AlsConfig (cp_als.hpp:32-40), plus one GPU-only field appended:
+ * dimtree = 1 runs each sweep as a dimension tree (PAPER.md
+ * 759-762): the modes split into a left and a right half, one pass over the
+ * tensor per half forms the half's partial MTTKRP (the other half's KRP
+ * contracted away), and every mode of the half takes its MTTKRP from that
+ * partial with a multi-TTV. Same updates in the same order as the reference
+ * sweep (a partial only involves factors not updated while it is in use);
+ * two tensor passes per iteration instead of N. 0 (zero-initialised callers)
+ * keeps the reference's one MTTKRP per mode. */
 typedef struct {
     int64_t rank;
     int max_iters;
@@ -124,6 +132,7 @@ typedef struct {
     int threads;
     int algo;
     int order;
+    int dimtree;
 } dmtk_gpu_als_config;
 
 /* dmtk::cp_als (cp_als.hpp:83): KruskalModel::random init (same mt19937_64

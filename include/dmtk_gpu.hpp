@@ -215,12 +215,14 @@ inline FactorMatrix solve_psd(const GramMatrix& h, const FactorMatrix& m) {
 /// dmtk::cp_als (cp_als.hpp:83). Per-iteration records carry the fit value
 /// and the device-timed seconds (mode_time[n].total is the mode's MTTKRP +
 /// solve time).
-inline AlsResult cp_als(const DenseTensor& x, const AlsConfig& config) {
+// dimension_tree (GPU-only, default off = the reference's sweep): see
+// dmtk_gpu_als_config.dimtree in dmtk_gpu.h.
+inline AlsResult cp_als(const DenseTensor& x, const AlsConfig& config, bool dimension_tree = false) {
     const dmtk_gpu_tensor h = handle(x);
     const auto& shape = x.shape();
     const int N = static_cast<int>(shape.ndim());
     dmtk_gpu_als_config c{config.rank, config.max_iters, config.tol, config.seed, config.threads,
-                          static_cast<int>(config.algo), static_cast<int>(config.order)};
+                          static_cast<int>(config.algo), static_cast<int>(config.order), dimension_tree ? 1 : 0};
     std::int64_t ftot = 0;
     for (int n = 0; n < N; ++n) ftot += shape.dim(n) * std::max<std::int64_t>(config.rank, 1);
     std::vector<double> f(static_cast<std::size_t>(std::max<std::int64_t>(ftot, 1)));

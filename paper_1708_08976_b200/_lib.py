@@ -35,7 +35,7 @@ class Times(C.Structure):
 
 class AlsConfig(C.Structure):
     _fields_ = [("rank", C.c_int64), ("max_iters", C.c_int), ("tol", C.c_double), ("seed", C.c_uint64),
-                ("threads", C.c_int), ("algo", C.c_int), ("order", C.c_int)]
+                ("threads", C.c_int), ("algo", C.c_int), ("order", C.c_int), ("dimtree", C.c_int)]
 
 
 T = C.c_void_p  # dmtk_gpu_tensor

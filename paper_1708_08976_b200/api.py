@@ -334,6 +334,9 @@ class AlsConfig:
     threads: int = 1
     algo: MttkrpAlgo = MttkrpAlgo.automatic
     order: TwoStepOrder = TwoStepOrder.automatic
+    # GPU-only: dimension-tree sweep (two tensor passes per iteration, see
+    # include/dmtk_gpu.h); False keeps the reference's one MTTKRP per mode
+    dimension_tree: bool = False
 
 
 @dataclass
@@ -372,7 +375,7 @@ def cp_als(x: DenseTensor, config: AlsConfig) -> AlsResult:
     dims = x.dims
     n = len(dims)
     cfg = _lib.AlsConfig(config.rank, config.max_iters, config.tol, config.seed, config.threads,
-                         int(config.algo), int(config.order))
+                         int(config.algo), int(config.order), int(bool(config.dimension_tree)))
     ftot = int(sum(dims)) * max(int(config.rank), 1)
     f = np.zeros(ftot)
     lam = np.zeros(max(int(config.rank), 1))

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -125,7 +126,7 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
     std::recursive_mutex mu;
-    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts;
+    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv;
     int* flag = nullptr;
     Context() = default;
 };
@@ -625,6 +626,75 @@ static int resolve_algo(int algo, int mode, int N) {
 static void krp_materialize(const std::vector<const double*>& U, const std::vector<long long>& rows, int C, double* out,
                             DevBuf& scratch, cudaStream_t s);
 
+// Streaming MTTKRP (or the generic fallback) of a planned view, then the
+// deterministic slot reduction into dout (out_rows x C, row-major).
+static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int kind, const KrpGen& bgen,
+                            const KrpGen& sgen, const double* X, int C, int csr_key, int mode, double* dout,
+                            cudaStream_t s, Phases* ph) {
+    CsrPlan& csr = csr_for(t, csr_key, C, mp, ctx);
+    ctx.ws.ensure(static_cast<size_t>(mp.ws_doubles));
+    if (mp.kind == kGeneric) {
+        // the generic kernel indexes KL over l and KR over j directly
+        const KrpGen kl = (kind == kTcM) ? sgen : bgen;
+        const KrpGen kr = (kind == kTcM) ? bgen : sgen;
+        launch_mttkrp_generic(X, mp.L, mp.I, mp.R, C, kl, kr, mp.jchunk, mp.n_jc, ctx.ws.p, s);
+        check_launch("mttkrp_generic");
+    } else {
+        mp.tc.bgen = bgen;
+        mp.tc.sgen = sgen;
+        mp.tc.ws = ctx.ws.p;
+        // small fastest factor: stage it in shared memory (builders read LDS)
+        // with a row pitch = 2 (mod 4) doubles (conflict-free fragment rows)
+        mp.tc.u0_pitch = 0;
+        {
+            const int P = C + ((6 - C % 4) % 4);
+            const long long bytes = bgen.ext[0] * P * 8;
+            const int padded = static_cast<int>((bytes + 127) / 128 * 128);
+            if (bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
+                !std::getenv("DMTK_GPU_NO_U0_SMEM")) {
+                mp.tc.u0_pitch = P;
+                mp.tc.smem += padded;
+            }
+        }
+        // heads = KRP of every B factor but the fastest (the reuse partial of
+        // krp.cpp:53-88), materialised once so a builder's head is one row load
+        mp.tc.htab = nullptr;
+        mp.tc.hrows = 0;
+        if (bgen.nf >= 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0) {
+            std::vector<const double*> in;
+            std::vector<long long> rows;
+            long long hr = 1;
+            for (int f = bgen.nf - 1; f >= 1; --f) {
+                in.push_back(bgen.U[f]);
+                rows.push_back(bgen.ext[f]);
+                hr *= bgen.ext[f];
+            }
+            ctx.htab.ensure(static_cast<size_t>(hr * C));
+            krp_materialize(in, rows, C, ctx.htab.p, ctx.scratch2, s);
+            mp.tc.htab = ctx.htab.p;
+            mp.tc.hrows = hr;
+        }
+
+        if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
+        static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;
+        if (plan_log)
+            std::fprintf(stderr,
+                         "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
+                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f\n",
+                         mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
+                         mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
+                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost);
+        const CUtensorMap map = make_map(X, mp);
+        if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
+            fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
+        check_launch("mttkrp_tc");
+    }
+    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
+    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s);
+    check_launch("slot_reduce");
+    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
+}
+
 static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
                            int order, double* dout, cudaStream_t s, Phases* ph) {
     const int N = static_cast<int>(t.dims.size());
@@ -754,68 +824,8 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
 
     ModePlan mp = have_pre ? pre : plan_mode(vdims, vmode, C, kind, ctx.sms);
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
-    CsrPlan& csr = csr_for(t, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0), C, mp, ctx);
-    ctx.ws.ensure(static_cast<size_t>(mp.ws_doubles));
-    if (mp.kind == kGeneric) {
-        // the generic kernel indexes KL over l and KR over j directly
-        const KrpGen kl = (kind == kTcM) ? sgen : bgen;
-        const KrpGen kr = (kind == kTcM) ? bgen : sgen;
-        launch_mttkrp_generic(X, mp.L, mp.I, mp.R, C, kl, kr, mp.jchunk, mp.n_jc, ctx.ws.p, s);
-        check_launch("mttkrp_generic");
-    } else {
-        mp.tc.bgen = bgen;
-        mp.tc.sgen = sgen;
-        mp.tc.ws = ctx.ws.p;
-        // small fastest factor: stage it in shared memory (builders read LDS)
-        // with a row pitch = 2 (mod 4) doubles (conflict-free fragment rows)
-        mp.tc.u0_pitch = 0;
-        {
-            const int P = C + ((6 - C % 4) % 4);
-            const long long bytes = bgen.ext[0] * P * 8;
-            const int padded = static_cast<int>((bytes + 127) / 128 * 128);
-            if (bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
-                !std::getenv("DMTK_GPU_NO_U0_SMEM")) {
-                mp.tc.u0_pitch = P;
-                mp.tc.smem += padded;
-            }
-        }
-        // heads = KRP of every B factor but the fastest (the reuse partial of
-        // krp.cpp:53-88), materialised once so a builder's head is one row load
-        mp.tc.htab = nullptr;
-        mp.tc.hrows = 0;
-        if (bgen.nf >= 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0) {
-            std::vector<const double*> in;
-            std::vector<long long> rows;
-            long long hr = 1;
-            for (int f = bgen.nf - 1; f >= 1; --f) {
-                in.push_back(bgen.U[f]);
-                rows.push_back(bgen.ext[f]);
-                hr *= bgen.ext[f];
-            }
-            ctx.htab.ensure(static_cast<size_t>(hr * C));
-            krp_materialize(in, rows, C, ctx.htab.p, ctx.scratch2, s);
-            mp.tc.htab = ctx.htab.p;
-            mp.tc.hrows = hr;
-        }
-
-        if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
-        static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;
-        if (plan_log)
-            std::fprintf(stderr,
-                         "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
-                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f\n",
-                         mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
-                         mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
-                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost);
-        const CUtensorMap map = make_map(X, mp);
-        if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
-            fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
-        check_launch("mttkrp_tc");
-    }
-    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
-    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s);
-    check_launch("slot_reduce");
-    if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
+    enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0),
+                    mode, dout, s, ph);
 }
 
 static void fill_times(Context& ctx, int algo, int mode, int N, dmtk_gpu_times* tm, double wall) {
@@ -1313,47 +1323,113 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
             check_launch("gram");
         }
-        // one mode of als_iterate (cp_als.cpp:134-153): MTTKRP, Gram-Hadamard
-        // from the cached Grams, solve, normalise, refresh this mode's Gram
-        auto mode_step = [&](int n) {
-            mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
-            const int nl = launch_als_update(grams, N, C, n, H, M.p, t->dims[n], Um[n], lam,
+        // ALS factor update from a mode's MTTKRP Mn (cp_als.cpp:134-153):
+        // Gram-Hadamard from the cached Grams, solve, normalise, refresh this
+        // mode's Gram. The fit reads the last mode's M (cp_als.cpp:149-155).
+        const double* fitM = M.p;
+        auto als_upd = [&](int n, const double* Mn) {
+            const int nl = launch_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam,
                                              grams + static_cast<long long>(n) * C * C, solve_scr, ctx.flag, s);
             count_launch(nl - 1);
             check_launch("als_update");
+            if (n == N - 1) fitM = Mn;
         };
-        // H and M still hold the last mode's values (cp_als.cpp:149-155)
+        auto mode_step = [&](int n) {
+            mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
+            als_upd(n, M.p);
+        };
+        // Dimension tree (dmtk_gpu.h, dimtree): halves [0, h) and [h, N)
+        const bool tree = cfg->dimtree != 0 && N >= 3;
+        int hsplit = 0;
+        DevBuf Pbuf;
+        if (tree) {
+            long long best = -1;
+            for (int h = 1; h < N; ++h) {
+                const long long m = std::max(prod(t->dims, 0, h), prod(t->dims, h, N));
+                if (best < 0 || m < best) {
+                    best = m;
+                    hsplit = h;
+                }
+            }
+            Pbuf.ensure(static_cast<size_t>(best * C));
+        }
+        const long long rowsL = tree ? prod(t->dims, 0, hsplit) : 0, rowsR = tree ? prod(t->dims, hsplit, N) : 0;
+        // left partial: every left row against the right half's KRP (M-major,
+        // the rows (i_0 .. i_{h-1}) kept); right partial: every right row
+        // against the (already updated) left half's KRP (K-major)
+        auto pass_left = [&]() {
+            const ModePlan mp = plan_view(1, rowsL, rowsR, C, kTcM, 0, ctx.sms);
+            const KrpGen bg = make_gen(t->dims, hsplit, N, Uc.data(), C, ctx.ones.p);
+            const KrpGen sg = make_gen(t->dims, 0, 0, Uc.data(), C, ctx.ones.p);
+            enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
+        };
+        auto pass_right = [&]() {
+            const ModePlan mp = plan_view(rowsL, rowsR, 1, C, kTcKJ, 0, ctx.sms);
+            const KrpGen bg = make_gen(t->dims, 0, hsplit, Uc.data(), C, ctx.ones.p);
+            const KrpGen sg = make_gen(t->dims, N, N, Uc.data(), C, ctx.ones.p);
+            enqueue_planned(*t, ctx, mp, kTcKJ, bg, sg, t->d, C, (300 + hsplit) * 128 + 1, -1, Pbuf.p, s, nullptr);
+        };
+        // mode k of the half [lo, hi) from its partial (multi-TTV)
+        auto half_step = [&](int k, int lo, int hi) {
+            if (hi - lo == 1) {
+                als_upd(k, Pbuf.p);
+                return;
+            }
+            const long long A = prod(t->dims, lo, k), dt = t->dims[k], B = prod(t->dims, k + 1, hi);
+            const KrpGen kl = make_gen(t->dims, lo, k, Uc.data(), C, ctx.ones.p);
+            const KrpGen kr = make_gen(t->dims, k + 1, hi, Uc.data(), C, ctx.ones.p);
+            ctx.mttv.ensure(static_cast<size_t>(multittv_ws_doubles(A, dt, B, C)));
+            launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
+            count_launch(1);
+            check_launch("multittv");
+            als_upd(k, M.p);
+        };
+        struct Step {
+            std::function<void()> fn;
+            int mode;
+        };
+        std::vector<Step> steps;
+        if (!tree) {
+            for (int n = 0; n < N; ++n) steps.push_back({[&, n] { mode_step(n); }, n});
+        } else {
+            steps.push_back({pass_left, 0});
+            for (int k = 0; k < hsplit; ++k) steps.push_back({[&, k] { half_step(k, 0, hsplit); }, k});
+            steps.push_back({pass_right, hsplit});
+            for (int k = hsplit; k < N; ++k) steps.push_back({[&, k] { half_step(k, hsplit, N); }, k});
+        }
         auto fit_step = [&]() {
-            launch_fit_cached(Um[N - 1], M.p, t->dims[N - 1], C, lam, H, grams + static_cast<long long>(N - 1) * C * C,
+            launch_fit_cached(Um[N - 1], fitM, t->dims[N - 1], C, lam, H, grams + static_cast<long long>(N - 1) * C * C,
                               dnorm, fitb, s);
             check_launch("fit");
         };
+        steps.push_back({fit_step, -1});
+        const int NS = static_cast<int>(steps.size());  // the last one is the fit
         // Iteration 1 runs eagerly (it builds every plan, CSR map and buffer);
-        // the later ones replay per-mode CUDA graphs of the same launches.
-        std::vector<cudaGraphExec_t> gexec(static_cast<size_t>(N + 1), nullptr);
-        std::vector<long long> gkernels(static_cast<size_t>(N + 1), 0);
+        // the later ones replay one CUDA graph per step of the same launches.
+        std::vector<cudaGraphExec_t> gexec(static_cast<size_t>(NS), nullptr);
+        std::vector<long long> gkernels(static_cast<size_t>(NS), 0);
         bool graphs = false;
-        std::vector<cudaEvent_t> evs(static_cast<size_t>(std::max(iters, 1)) * (N + 1));
+        std::vector<cudaEvent_t> evs(static_cast<size_t>(std::max(iters, 1)) * NS);
         for (auto& e : evs) CK(cudaEventCreate(&e));
         std::vector<double> f4(4 * fit_slots, 0.0);
         double prev_fit = 0.0;
         int done = 0;
         for (int iter = 1; iter <= iters; ++iter) {
-            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * (N + 1);
-            for (int n = 0; n <= N; ++n) {
-                if (n < N) CK(cudaEventRecord(ev[n], s));
+            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * NS;
+            for (int st = 0; st < NS; ++st) {
+                if (st < NS - 1) CK(cudaEventRecord(ev[st], s));
                 if (graphs) {
-                    CK(cudaGraphLaunch(gexec[n], s));
-                    count_launch(static_cast<int>(gkernels[n]));
+                    CK(cudaGraphLaunch(gexec[st], s));
+                    count_launch(static_cast<int>(gkernels[st]));
                 } else {
-                    n < N ? mode_step(n) : fit_step();
+                    steps[st].fn();
                 }
-                if (n == N - 1) CK(cudaEventRecord(ev[N], s));
+                if (st == NS - 2) CK(cudaEventRecord(ev[NS - 1], s));
             }
             CK(cudaMemcpyAsync(fitb + 4 * iter, fitb, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
             if (iter == 1 && iters > 1) {  // capture after the eager warm-up iteration
                 bool ok = true;
-                for (int n = 0; n <= N && ok; ++n) {
+                for (int st = 0; st < NS && ok; ++st) {
                     cudaGraph_t g = nullptr;
                     const long long before = g_launches.load();
                     if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
@@ -1361,15 +1437,16 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
                         break;
                     }
                     try {
-                        n < N ? mode_step(n) : fit_step();
+                        steps[st].fn();
                     } catch (const Err&) {
                         ok = false;
                     }
                     const cudaError_t ec = cudaStreamEndCapture(s, &g);
-                    if (!ok || ec != cudaSuccess || !g || cudaGraphInstantiate(&gexec[n], g, 0) != cudaSuccess) ok = false;
+                    if (!ok || ec != cudaSuccess || !g || cudaGraphInstantiate(&gexec[st], g, 0) != cudaSuccess)
+                        ok = false;
                     if (g) cudaGraphDestroy(g);
-                    gkernels[n] = g_launches.load() - before;
-                    g_launches.fetch_sub(gkernels[n]);  // captured, not launched
+                    gkernels[st] = g_launches.load() - before;
+                    g_launches.fetch_sub(gkernels[st]);  // captured, not launched
                 }
                 cudaGetLastError();
                 graphs = ok;
@@ -1391,12 +1468,14 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         CK(cudaMemcpyAsync(f4.data(), fitb, 4 * fit_slots * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         for (int iter = 1; iter <= done; ++iter) {
-            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * (N + 1);
+            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * NS;
             float ms_total = 0;
-            for (int n = 0; n < N; ++n) {
+            if (mode_seconds_out)
+                for (int n = 0; n < N; ++n) mode_seconds_out[(iter - 1) * N + n] = 0.0;
+            for (int st = 0; st < NS - 1; ++st) {  // a tree pass counts toward the first mode of its half
                 float ms;
-                CK(cudaEventElapsedTime(&ms, ev[n], n + 1 < N ? ev[n + 1] : ev[N]));
-                if (mode_seconds_out) mode_seconds_out[(iter - 1) * N + n] = ms * 1e-3;
+                CK(cudaEventElapsedTime(&ms, ev[st], ev[st + 1]));
+                if (mode_seconds_out) mode_seconds_out[(iter - 1) * N + steps[st].mode] += ms * 1e-3;
                 ms_total += ms;
             }
             if (iter_seconds_out) iter_seconds_out[iter - 1] = ms_total * 1e-3;

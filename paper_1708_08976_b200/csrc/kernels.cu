@@ -62,6 +62,53 @@ __global__ void __launch_bounds__(256) krp_level_kernel(const double* __restrict
     }
 }
 
+// ----------------------------------------------- multi-TTV over a partial
+// Dimension-tree CP-ALS: a half's partial MTTKRP P (rows over the half's
+// modes, row-major rows x C) gives the MTTKRP of one of its modes t:
+//   M(i, c) = sum_{a < A, b < B} P(a + A (i + d_t b), c) KL(a, c) KR(b, c)
+// (KL/KR the KRPs of the half's modes before/after t, the multi-TTV of the
+// paper's 2-step, mttkrp.cpp:350-356). Grid (d_t, S): block (i, s) sums its
+// chunk of the (a, b) terms with thread (p, c) striding by P parts, parts
+// added in a fixed order; a second kernel adds the S chunks in order.
+__global__ void __launch_bounds__(256) multittv_partial_kernel(const double* __restrict__ P, int C, long long A,
+                                                               long long dt, long long B, KrpGen kl, KrpGen kr,
+                                                               long long per_chunk, double* __restrict__ ws) {
+    __shared__ double red[256];
+    const long long i = blockIdx.x;
+    const long long s = blockIdx.y;
+    const long long T = A * B;
+    const long long t0 = s * per_chunk;
+    const long long t1 = t0 + per_chunk < T ? t0 + per_chunk : T;
+    const int parts = blockDim.x / C;
+    const int p = threadIdx.x / C;
+    const int c = threadIdx.x - p * C;
+    double acc = 0.0;
+    if (p < parts) {
+        for (long long tau = t0 + p; tau < t1; tau += parts) {
+            const long long b = div_nn(tau, A);
+            const long long a = tau - b * A;
+            const long long row = a + A * (i + dt * b);
+            acc += P[row * C + c] * krp_value(kl, a, c) * krp_value(kr, b, c);
+        }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < C) {
+        double t = 0.0;
+        for (int q = 0; q < parts; ++q) t += red[q * C + threadIdx.x];
+        ws[(s * dt + i) * C + threadIdx.x] = t;
+    }
+}
+
+__global__ void multittv_final_kernel(const double* __restrict__ ws, int S, long long dt, int C,
+                                      double* __restrict__ M) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= dt * C) return;
+    double t = 0.0;
+    for (int s = 0; s < S; ++s) t += ws[s * dt * C + e];
+    M[e] = t;
+}
+
 // ----------------------------------------------------------- generic MTTKRP
 // M(i,c) partial over a chunk of j: sum_j KR(j,c) * sum_l X(l,i,j) KL(l,c).
 // Slot layout ws[(jc * I + i) * C + c]; the CSR reduce finishes the sum.
@@ -670,6 +717,25 @@ void launch_mttkrp_generic(const double* X, long long L, long long I, long long 
                            const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(n_jc), static_cast<unsigned>((I * C + 127) / 128));
     mttkrp_generic_kernel<<<grid, 128, 0, s>>>(X, L, I, R, C, kl, kr, jchunk, ws);
+}
+
+long long multittv_ws_doubles(long long A, long long dt, long long B, int C) {
+    const long long T = A * B;
+    long long S = (2 * 148 + dt - 1) / dt;
+    S = std::max<long long>(1, std::min<long long>(S, std::max<long long>(1, T / 32)));
+    return S * dt * C;
+}
+
+void launch_multittv(const double* P, int C, long long A, long long dt, long long B, const KrpGen& kl,
+                     const KrpGen& kr, double* ws, double* M, cudaStream_t s) {
+    const long long T = A * B;
+    long long S = (2 * 148 + dt - 1) / dt;
+    S = std::max<long long>(1, std::min<long long>(S, std::max<long long>(1, T / 32)));
+    const long long per = (T + S - 1) / S;
+    multittv_partial_kernel<<<dim3(static_cast<unsigned>(dt), static_cast<unsigned>(S)), 256, 0, s>>>(
+        P, C, A, dt, B, kl, kr, per, ws);
+    const long long n = dt * C;
+    multittv_final_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, static_cast<int>(S), dt, C, M);
 }
 
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,

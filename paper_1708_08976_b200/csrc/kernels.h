@@ -11,6 +11,11 @@ void launch_krp_level(const double* P, const double* U, double* out, long long r
                       cudaStream_t s);
 void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,
                            const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s);
+// Multi-TTV of a dimension-tree partial (see kernels.cu): M (dt x C) from P
+// over rows a + A (i + dt b); ws holds multittv_ws_doubles(...) doubles.
+long long multittv_ws_doubles(long long A, long long dt, long long B, int C);
+void launch_multittv(const double* P, int C, long long A, long long dt, long long B, const KrpGen& kl,
+                     const KrpGen& kr, double* ws, double* M, cudaStream_t s);
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
                         double* out, cudaStream_t s);
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s);

@@ -70,9 +70,9 @@ def test_krp_config1_product(oracle):
     assert np.array_equal(got[r], (ins[0][d0] * ins[1][d1]) * ins[2][d2])
 
 
-def cp(x, dims, rank, iters, seed, tol=0.0, algo=A.automatic):
+def cp(x, dims, rank, iters, seed, tol=0.0, algo=A.automatic, tree=False):
     t = dg.DenseTensor(dims, x)
-    return dg.cp_als(t, AlsConfig(rank=rank, max_iters=iters, tol=tol, seed=seed, algo=algo))
+    return dg.cp_als(t, AlsConfig(rank=rank, max_iters=iters, tol=tol, seed=seed, algo=algo, dimension_tree=tree))
 
 
 @pytest.mark.parametrize("dims,rank,iters", [((6, 5, 4), 3, 6), ((7, 6, 5), 3, 8), ((8, 9, 10), 4, 40),
@@ -88,6 +88,24 @@ def test_cp_als_fits_match_reference(ref, oracle, dims, rank, iters):
     for u in got.model.factors:  # final factors column-normalised (test_cpals.cpp:157-167)
         assert np.allclose(np.linalg.norm(u, axis=0), 1.0, rtol=1e-12, atol=0)
     assert np.all(got.model.lambda_ >= 0)
+
+
+@pytest.mark.parametrize("dims,rank,iters", [((6, 5, 4), 3, 6), ((8, 9, 10), 4, 40), ((12, 10, 8, 6), 5, 10),
+                                             ((40, 40, 12, 8), 20, 25), ((5, 4, 3, 2, 6), 4, 12),
+                                             ((9, 3, 4, 2, 2, 5), 6, 10)])
+def test_cp_als_dimension_tree_matches_reference(ref, oracle, dims, rank, iters):
+    """Dimension-tree sweep (two tensor passes per iteration):
+    the same updates as the reference's per-mode sweep, fits within 1e-9."""
+    x = oracle.gen_tensor(dims, 31)
+    got = cp(x, dims, rank, iters, 7, tree=True)
+    want = ref.cp_als(x, dims, rank, iters, tol=0.0, seed=7)
+    f_got = np.array([r.fit.fit for r in got.trace.iters])
+    assert len(f_got) == len(want["fits"])
+    assert np.max(np.abs(f_got - want["fits"])) <= 1e-9
+    for u in got.model.factors:
+        assert np.allclose(np.linalg.norm(u, axis=0), 1.0, rtol=1e-12, atol=0)
+    again = cp(x, dims, rank, iters, 7, tree=True)  # deterministic
+    assert [r.fit.fit for r in again.trace.iters] == list(f_got)
 
 
 def test_cp_als_monotone_and_deterministic(oracle):

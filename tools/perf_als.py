@@ -33,17 +33,18 @@ def main():
     ap.add_argument("--dims", default="100,100,1200,80")
     ap.add_argument("--rank", type=int, default=20)
     ap.add_argument("--iters", type=int, default=25)
+    ap.add_argument("--tree", action="store_true", help="dimension-tree sweep (two tensor passes per iteration)")
     args = ap.parse_args()
     dims = tuple(int(d) for d in args.dims.split(","))
     x = fmri_tensor(dims)
     t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
-    dg.cp_als(t, dg.AlsConfig(rank=args.rank, max_iters=2, tol=0.0, seed=1))  # warm-up (plans)
+    dg.cp_als(t, dg.AlsConfig(rank=args.rank, max_iters=2, tol=0.0, seed=1, dimension_tree=args.tree))  # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = dg.cp_als(t, dg.AlsConfig(rank=args.rank, max_iters=args.iters, tol=0.0, seed=1))
+    res = dg.cp_als(t, dg.AlsConfig(rank=args.rank, max_iters=args.iters, tol=0.0, seed=1, dimension_tree=args.tree))
     wall = time.perf_counter() - t0
     per_iter = [r.total_seconds for r in res.trace.iters]
-    print(json.dumps({"dims": dims, "rank": args.rank, "iters": len(per_iter), "wall_s": round(wall, 4),
+    print(json.dumps({"dims": dims, "rank": args.rank, "tree": args.tree, "iters": len(per_iter), "wall_s": round(wall, 4),
                       "iter_ms_median": round(1e3 * sorted(per_iter)[len(per_iter) // 2], 3),
                       "mode_ms_iter1": [round(1e3 * v, 3) for v in res.trace.iters[-1].mode_time],
                       "final_fit": res.trace.iters[-1].fit.fit, "tensor_norm": res.trace.tensor_norm}))
