@@ -126,7 +126,7 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
     std::recursive_mutex mu;
-    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv;
+    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv, u0pad;
     int* flag = nullptr;
     Context() = default;
 };
@@ -196,8 +196,14 @@ struct CsrPlan {
 
 struct dmtk_gpu_tensor_s {
     int device = 0;
-    std::vector<long long> dims;
+    std::vector<long long> dims;  // logical extents (the reference's Shape)
     long long total = 0;
+    // physical layout on the device: an uploaded tensor whose first extent is
+    // odd is stored with one zero slice appended in mode 0, so every
+    // collapsed view has 16-byte strides (TMA); the first factor then carries
+    // a zero row and mode-0 results are truncated (adding exact zeros).
+    std::vector<long long> pdims;
+    long long ptotal = 0;
     const double* d = nullptr;
     bool owned = false;
     std::mutex mu;
@@ -380,10 +386,14 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
     mp.tail = tail;
     const long long lim = (1LL << 31) - 1;
     bool ok = rank_ok;
+    // strides TMA cannot describe (not 16-byte multiples) use the LDGSTS producer
+    int ldgsts = 0;
     if (kind_req == kTcM) {
-        ok = ok && (mp.L * mp.I) % 2 == 0 && mp.L * mp.I <= lim && mp.R <= lim;
+        ok = ok && mp.L * mp.I <= lim && mp.R <= lim;
+        ldgsts = (mp.L * mp.I) % 2 != 0;
     } else if (kind_req == kTcKJ || kind_req == kTcKJK) {
-        ok = ok && mp.L % 2 == 0 && mp.L <= lim && mp.I <= lim && mp.R <= lim;
+        ok = ok && mp.L <= lim && mp.I <= lim && mp.R <= lim;
+        ldgsts = mp.L % 2 != 0;
     }
     mp.kind = ok ? kind_req : kGeneric;
     if (mp.kind == kGeneric) {
@@ -401,6 +411,7 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
     p.I = mp.I;
     p.R = mp.R;
     p.swap = swap;
+    p.ldgsts = ldgsts;
     if (swap) mp.out_rows = kind_req == kTcM ? mp.L : mp.R;
     Tiling tl;
     double tcost = 1e300;
@@ -560,6 +571,10 @@ static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& m
     auto plan = std::make_unique<CsrPlan>();
     plan->rows = mp.out_rows;
     std::vector<long long> rowptr(mp.out_rows + 1, 0), slots(pairs.size());
+    pairs.erase(std::remove_if(pairs.begin(), pairs.end(),
+                               [&](const std::pair<long long, long long>& pr) { return pr.first >= mp.out_rows; }),
+                pairs.end());  // slots of padding rows
+    slots.resize(pairs.size());
     for (auto& pr : pairs) ++rowptr[pr.first + 1];
     for (long long i = 0; i < mp.out_rows; ++i) rowptr[i + 1] += rowptr[i];
     std::vector<long long> fill(rowptr.begin(), rowptr.end() - 1);
@@ -676,15 +691,23 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         }
 
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
+        mp.tc.X = X;
+        static const bool force_ldgsts = std::getenv("DMTK_GPU_FORCE_LDGSTS") != nullptr;
+        if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || force_ldgsts) mp.tc.ldgsts = 1;
         static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;
         if (plan_log)
             std::fprintf(stderr,
                          "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
-                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f\n",
+                         "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f "
+                         "ldgsts %d\n",
                          mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
                          mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
-                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost);
-        const CUtensorMap map = make_map(X, mp);
+                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost, mp.tc.ldgsts);
+        CUtensorMap map;
+        if (mp.tc.ldgsts)
+            std::memset(&map, 0, sizeof(map));
+        else
+            map = make_map(X, mp);
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
             fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
         check_launch("mttkrp_tc");
@@ -698,7 +721,7 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
 static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
                            int order, double* dout, cudaStream_t s, Phases* ph) {
     const int N = static_cast<int>(t.dims.size());
-    const auto& dims = t.dims;
+    const auto& dims = t.pdims;  // physical layout (mode 0 possibly padded)
     algo = resolve_algo(algo, mode, N);
     const bool boundary = (mode == 0 || mode == N - 1);
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[0], s));
@@ -724,7 +747,7 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
         const long long L = prod(dims, 0, mode), I = dims[mode], R = prod(dims, mode + 1, N);
         const long long unfold = L * R;
         if (!boundary) {
-            ctx.reorder.ensure(static_cast<size_t>(t.total));
+            ctx.reorder.ensure(static_cast<size_t>(t.ptotal));
             launch_matricize(X, L, I, R, ctx.reorder.p, s);
             check_launch("matricize");
             X = ctx.reorder.p;
@@ -823,6 +846,7 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
     }
 
     ModePlan mp = have_pre ? pre : plan_mode(vdims, vmode, C, kind, ctx.sms);
+    if (mode == 0) mp.out_rows = std::min(mp.out_rows, t.dims[0]);  // drop a pad row
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
     enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0),
                     mode, dout, s, ph);
@@ -915,19 +939,23 @@ static void inject_fault(double* m, long long n) {
 }
 
 // Upload host factors into ctx.fac; fill device pointer table.
+// (physical rows: the first factor of a padded tensor gets a zero row)
 static void upload_factors(Context& ctx, const dmtk_gpu_tensor_s& t, const double* const* factors, long long C,
                            std::vector<const double*>& dptr) {
     const int N = static_cast<int>(t.dims.size());
     long long tot = 0;
-    for (int k = 0; k < N; ++k) tot += t.dims[k] * C;
+    for (int k = 0; k < N; ++k) tot += t.pdims[k] * C;
     ctx.fac.ensure(static_cast<size_t>(tot));
     dptr.resize(N);
     long long off = 0;
     for (int k = 0; k < N; ++k) {
         CK(cudaMemcpyAsync(ctx.fac.p + off, factors[k], static_cast<size_t>(t.dims[k] * C) * sizeof(double),
                            cudaMemcpyHostToDevice, ctx.stream));
+        if (t.pdims[k] != t.dims[k])
+            CK(cudaMemsetAsync(ctx.fac.p + off + t.dims[k] * C, 0,
+                               static_cast<size_t>((t.pdims[k] - t.dims[k]) * C) * sizeof(double), ctx.stream));
         dptr[k] = ctx.fac.p + off;
-        off += t.dims[k] * C;
+        off += t.pdims[k] * C;
     }
 }
 
@@ -945,7 +973,7 @@ struct AlsOut {
 static double tensor_norm_dev(dmtk_gpu_tensor_s& t, Context& ctx) {
     const int parts = ctx.sms * 4;
     ctx.norm_parts.ensure(parts + 1);
-    launch_tensor_norm(t.d, t.total, ctx.norm_parts.p, parts, ctx.norm_parts.p + parts, ctx.stream);
+    launch_tensor_norm(t.d, t.ptotal, ctx.norm_parts.p, parts, ctx.norm_parts.p + parts, ctx.stream);
     count_launch(2);
     ck(cudaGetLastError(), "tensor_norm");
     double v = 0;
@@ -1003,13 +1031,27 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
         t->device = device;
         t->dims = d;
         t->total = prod(d, 0, ndim);
+        t->pdims = d;
+        if (ndim > 0 && d[0] % 2 != 0 && t->total > 0) t->pdims[0] = d[0] + 1;
+        t->ptotal = prod(t->pdims, 0, ndim);
         double* p = nullptr;
         // stream-ordered pool allocation: repeated upload/free cycles reuse the
         // pool instead of paying cudaMalloc/cudaFree for every 8 GB tensor
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(t->total) * sizeof(double), ctx.stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(std::max<long long>(t->ptotal, 1)) *
+                                                             sizeof(double),
+                           ctx.stream));
         t->d = p;
         t->owned = true;
-        CK(cudaMemcpyAsync(p, host, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        if (t->pdims == t->dims) {
+            CK(cudaMemcpyAsync(p, host, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx.stream));
+        } else {  // pitched copy into the padded layout, zero pad slice
+            const size_t rows = static_cast<size_t>(t->total / d[0]);
+            const size_t pitch = static_cast<size_t>(t->pdims[0]) * sizeof(double);
+            CK(cudaMemcpy2DAsync(p, pitch, host, static_cast<size_t>(d[0]) * sizeof(double),
+                                 static_cast<size_t>(d[0]) * sizeof(double), rows, cudaMemcpyHostToDevice, ctx.stream));
+            CK(cudaMemset2DAsync(p + d[0], pitch, 0, sizeof(double), rows, ctx.stream));
+        }
         CK(cudaStreamSynchronize(ctx.stream));
         *out = t.release();
     });
@@ -1024,6 +1066,8 @@ int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double
         t->device = device;
         t->dims = d;
         t->total = prod(d, 0, ndim);
+        t->pdims = d;  // caller's layout: odd strides take the LDGSTS producer
+        t->ptotal = t->total;
         t->d = device_ptr;
         t->owned = false;
         *out = t.release();
@@ -1109,8 +1153,17 @@ int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factor
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
-        mttkrp_enqueue(*t, ctx, device_factors, static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out,
-                       s, nullptr);
+        std::vector<const double*> f(device_factors, device_factors + N);
+        if (t->pdims[0] != t->dims[0]) {  // padded tensor: first factor with a zero row
+            const size_t rowsz = static_cast<size_t>(rank) * sizeof(double);
+            ctx.u0pad.ensure(static_cast<size_t>(t->pdims[0] * rank));
+            CK(cudaMemcpyAsync(ctx.u0pad.p, f[0], static_cast<size_t>(t->dims[0]) * rowsz, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemsetAsync(ctx.u0pad.p + t->dims[0] * rank, 0, static_cast<size_t>(t->pdims[0] - t->dims[0]) * rowsz,
+                               s));
+            f[0] = ctx.u0pad.p;
+        }
+        mttkrp_enqueue(*t, ctx, f.data(), static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out, s,
+                       nullptr);
     });
 }
 
@@ -1278,13 +1331,20 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
 
         // KruskalModel::random (cp_als.cpp:87-99): one mt19937_64 stream
         std::mt19937_64 rng(cfg->seed);
-        long long ftot = 0, maxrows = 0;
+        long long ftot = 0, maxrows = 0, ptot = 0;  // logical / physical (padded first factor) sizes
         for (int k = 0; k < N; ++k) {
             ftot += t->dims[k] * C;
-            maxrows = std::max(maxrows, t->dims[k]);
+            ptot += t->pdims[k] * C;
+            maxrows = std::max(maxrows, t->pdims[k]);
         }
-        std::vector<double> hf(static_cast<size_t>(ftot));
-        for (auto& v : hf) v = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+        std::vector<double> hf(static_cast<size_t>(ptot), 0.0);
+        {
+            long long po = 0;
+            for (int k = 0; k < N; ++k) {  // reference stream order; pad rows stay zero
+                for (long long e = 0; e < t->dims[k] * C; ++e) hf[po + e] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+                po += t->pdims[k] * C;
+            }
+        }
 
         const double normx = tensor_norm_dev(*t, ctx);
         *tensor_norm_out = normx;
@@ -1298,7 +1358,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         }
         // device state: factors | lambda | M | H | Grams (N x C x C) | normx | fits | solve scratch
         DevBuf F, M, aux;
-        F.ensure(static_cast<size_t>(ftot));
+        F.ensure(static_cast<size_t>(ptot));
         M.ensure(static_cast<size_t>(maxrows * C));
         const int iters = cfg->max_iters;
         const int fit_slots = std::max(iters, 1) + 1;
@@ -1319,7 +1379,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         for (int k = 0; k < N; ++k) {
             Um[k] = F.p + off;
             Uc[k] = Um[k];
-            off += t->dims[k] * C;
+            off += t->pdims[k] * C;
             launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
             check_launch("gram");
         }
@@ -1345,7 +1405,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         if (tree) {
             long long best = -1;
             for (int h = 1; h < N; ++h) {
-                const long long m = std::max(prod(t->dims, 0, h), prod(t->dims, h, N));
+                const long long m = std::max(prod(t->pdims, 0, h), prod(t->pdims, h, N));
                 if (best < 0 || m < best) {
                     best = m;
                     hsplit = h;
@@ -1353,20 +1413,20 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             }
             Pbuf.ensure(static_cast<size_t>(best * C));
         }
-        const long long rowsL = tree ? prod(t->dims, 0, hsplit) : 0, rowsR = tree ? prod(t->dims, hsplit, N) : 0;
+        const long long rowsL = tree ? prod(t->pdims, 0, hsplit) : 0, rowsR = tree ? prod(t->pdims, hsplit, N) : 0;
         // left partial: every left row against the right half's KRP (M-major,
         // the rows (i_0 .. i_{h-1}) kept); right partial: every right row
         // against the (already updated) left half's KRP (K-major)
         auto pass_left = [&]() {
             const ModePlan mp = plan_view(1, rowsL, rowsR, C, kTcM, 0, ctx.sms);
-            const KrpGen bg = make_gen(t->dims, hsplit, N, Uc.data(), C, ctx.ones.p);
-            const KrpGen sg = make_gen(t->dims, 0, 0, Uc.data(), C, ctx.ones.p);
+            const KrpGen bg = make_gen(t->pdims, hsplit, N, Uc.data(), C, ctx.ones.p);
+            const KrpGen sg = make_gen(t->pdims, 0, 0, Uc.data(), C, ctx.ones.p);
             enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
         };
         auto pass_right = [&]() {
             const ModePlan mp = plan_view(rowsL, rowsR, 1, C, kTcKJ, 0, ctx.sms);
-            const KrpGen bg = make_gen(t->dims, 0, hsplit, Uc.data(), C, ctx.ones.p);
-            const KrpGen sg = make_gen(t->dims, N, N, Uc.data(), C, ctx.ones.p);
+            const KrpGen bg = make_gen(t->pdims, 0, hsplit, Uc.data(), C, ctx.ones.p);
+            const KrpGen sg = make_gen(t->pdims, N, N, Uc.data(), C, ctx.ones.p);
             enqueue_planned(*t, ctx, mp, kTcKJ, bg, sg, t->d, C, (300 + hsplit) * 128 + 1, -1, Pbuf.p, s, nullptr);
         };
         // mode k of the half [lo, hi) from its partial (multi-TTV)
@@ -1375,9 +1435,9 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
                 als_upd(k, Pbuf.p);
                 return;
             }
-            const long long A = prod(t->dims, lo, k), dt = t->dims[k], B = prod(t->dims, k + 1, hi);
-            const KrpGen kl = make_gen(t->dims, lo, k, Uc.data(), C, ctx.ones.p);
-            const KrpGen kr = make_gen(t->dims, k + 1, hi, Uc.data(), C, ctx.ones.p);
+            const long long A = prod(t->pdims, lo, k), dt = t->pdims[k], B = prod(t->pdims, k + 1, hi);
+            const KrpGen kl = make_gen(t->pdims, lo, k, Uc.data(), C, ctx.ones.p);
+            const KrpGen kr = make_gen(t->pdims, k + 1, hi, Uc.data(), C, ctx.ones.p);
             ctx.mttv.ensure(static_cast<size_t>(multittv_ws_doubles(A, dt, B, C)));
             launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
             count_launch(1);
@@ -1484,7 +1544,15 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         for (auto& ge : gexec)
             if (ge) cudaGraphExecDestroy(ge);
         for (auto& e : evs) cudaEventDestroy(e);
-        CK(cudaMemcpyAsync(factors_out, F.p, static_cast<size_t>(ftot) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        {
+            long long lo_ = 0, po = 0;  // logical rows only
+            for (int k = 0; k < N; ++k) {
+                CK(cudaMemcpyAsync(factors_out + lo_, F.p + po, static_cast<size_t>(t->dims[k] * C) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s));
+                lo_ += t->dims[k] * C;
+                po += t->pdims[k] * C;
+            }
+        }
         if (done > 0) {
             CK(cudaMemcpyAsync(lambda_out, lam, static_cast<size_t>(C) * sizeof(double), cudaMemcpyDeviceToHost, s));
         } else {

@@ -75,6 +75,9 @@ struct TcPlan {
     long long hrows;
     int smem;                 // dynamic shared memory bytes
     int u0_pitch;             // > 0: fastest B factor staged in shared memory with this row pitch
+    const double* X;          // tensor base (the LDGSTS producer reads it directly)
+    int ldgsts;               // 1: strides or base not 16-byte aligned for TMA; the producer warp
+                              // copies the swizzled stage with 8-byte cp.async instead
 };
 
 // Stage range of CTA b under the stream-K split.

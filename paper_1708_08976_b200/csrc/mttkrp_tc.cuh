@@ -113,12 +113,13 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1 + p.G);  // producer expect_tx + one builder item per row group
+            // producer (one expect_tx arrival, or 32 cp.async arrivals) + one per builder item
+            mbar_init(&full[s], (p.ldgsts ? 32 : 1) + p.G);
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_barrier_init();
     }
-    if (warp == kProducerWarp && lane == 0) tma_prefetch_desc(&tmap);
+    if (warp == kProducerWarp && lane == 0 && !p.ldgsts) tma_prefetch_desc(&tmap);
     __syncthreads();
 
     long long lo, hi;
@@ -126,6 +127,84 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     const long long spt = p.stages_per_tile;
 
     // ------------------------------------------------------------ producer
+    if (warp == kProducerWarp && p.ldgsts) {
+        // Strides (or the base) not 16-byte aligned: TMA cannot describe the
+        // view, so the whole warp copies each stage with 8-byte cp.async into
+        // the same 128-byte-swizzled box layout the TMA path produces (zero
+        // fill out of range), then arrives on the full barrier when its copies
+        // have landed.
+        StageCursor cur;
+        cur.init(lo, spt);
+        const double* __restrict__ X = p.X;
+        for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
+            const int slot = cur.slot;
+            const long long tile = cur.tile;
+            const long long st = cur.st;
+            mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
+            const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
+            if (!KMAJ) {
+                // lane-owned rows mm = lane + 32 q of every column: the smem row
+                // offset and the global pointer advance incrementally per column
+                const long long mrows = p.L * p.I;
+                const long long m0 = tile * p.TR;
+                const long long j0 = st * BK * G;
+                const int nq = (p.TR + 31) >> 5;
+                for (int q = 0; q < nq; ++q) {
+                    const int mm = lane + 32 * q;
+                    if (mm >= p.TR) break;
+                    const long long m = m0 + mm;
+                    const bool mok = m < mrows;
+                    const int w16 = mm & 15;
+                    const uint32_t wlo = (w16 & 1) << 3, whi = w16 >> 1;
+                    for (int gi = 0; gi < G; ++gi) {
+                        uint32_t d = dst + (gi * (p.TR / 16) + (mm >> 4)) * (128 * BK);
+                        long long j = j0 + BK * gi;
+                        const double* src = X + j * mrows + m;
+#pragma unroll 8
+                        for (int jj = 0; jj < BK; ++jj, d += 128, src += mrows, ++j) {
+                            const bool ok = mok && j < p.R;
+                            cp_async_8(d + (((whi ^ (jj & 7)) << 4) | wlo), ok ? src : X, ok ? 8u : 0u);
+                        }
+                    }
+                }
+            } else {
+                long long ti, tj, j, l0;
+                if (p.flavor == kKMajorJ) {
+                    tj = div_nn(tile, p.n_ti);
+                    ti = tile - tj * p.n_ti;
+                    l0 = st * BK * G;
+                    j = tj * p.BJ;
+                } else {
+                    ti = tile;
+                    j = div_nn(st, p.n_lc);
+                    l0 = (st - j * p.n_lc) * BK * G;
+                }
+                // lane = (row pair, l): 16 lanes per 128-byte row, two rows per pass
+                const int gbytes = Cfg::A_BYTES / G;
+                const int ll = lane & 15;
+                const uint32_t llo = (ll & 1) << 3, lhi = ll >> 1;
+                for (int rho = lane >> 4; rho < p.TR; rho += 2) {
+                    const int jl = rho / p.BI;
+                    const long long i = ti * p.BI + (rho - jl * p.BI);
+                    const long long jj = j + jl;
+                    const bool rok = i < p.I && jj < p.R;
+                    const double* row = X + p.L * (i + p.I * jj);
+                    const uint32_t roff = rho * 128 + ((lhi ^ (rho & 7)) << 4) + llo;
+                    for (int gi = 0; gi < G; ++gi) {
+#pragma unroll
+                        for (int h = 0; h < BK / 16; ++h) {
+                            const long long l = l0 + BK * gi + 16 * h + ll;
+                            const bool ok = rok && l < p.L;
+                            cp_async_8(dst + gi * gbytes + h * (gbytes / (BK / 16)) + roff, ok ? row + l : X,
+                                       ok ? 8u : 0u);
+                        }
+                    }
+                }
+            }
+            cp_async_mbar_arrive_noinc(full_a + 8 * slot);
+        }
+        return;
+    }
     if (warp == kProducerWarp) {
         if (lane == 0) {
             const uint64_t pol = (p.debug & 16) ? l2_evict_normal_policy() : l2_evict_first_policy();

@@ -21,6 +21,7 @@ CONFIGS = {
     "180c25": ((180, 180, 180, 180), 25),
     "64c32": ((64, 64, 64, 64, 64), 32),
     "fmri20": ((100, 100, 1200, 80), 20),
+    "odd25": ((999, 1001, 997), 25),
 }
 ALGOS = {"auto": (A.automatic, O.automatic), "one": (A.one_step, O.automatic), "left": (A.two_step, O.left),
          "right": (A.two_step, O.right), "base": (A.baseline, O.automatic)}
@@ -33,6 +34,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--bw", type=float, default=6455.9)
     ap.add_argument("--modes", default="")
+    ap.add_argument("--upload", action="store_true", help="upload through the host API (padded odd layouts)")
     args = ap.parse_args()
     peak = dg.fp64_peak_tflops()
     for cfg in args.config.split(","):
@@ -43,7 +45,8 @@ def main():
         g = torch.Generator(device="cuda").manual_seed(1)
         x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
         fs = [torch.rand((d, C), dtype=torch.float64, device="cuda", generator=g) for d in dims]
-        t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
+        t = (dg.DenseTensor(dims, x.cpu().numpy()) if args.upload else
+             dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x))
         s = torch.cuda.current_stream()
         modes = [int(m) for m in args.modes.split(",")] if args.modes else range(len(dims))
         for mode in modes:
