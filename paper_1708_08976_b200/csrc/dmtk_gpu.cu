@@ -126,7 +126,8 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
     std::recursive_mutex mu;
-    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv, u0pad;
+    DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv, u0pad,
+        chunk_fac, chunk_out;
     int* flag = nullptr;
     Context() = default;
 };
@@ -718,7 +719,7 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
 }
 
-static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
+static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
                            int order, double* dout, cudaStream_t s, Phases* ph) {
     const int N = static_cast<int>(t.dims.size());
     const auto& dims = t.pdims;  // physical layout (mode 0 possibly padded)
@@ -850,6 +851,40 @@ static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* con
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
     enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0),
                     mode, dout, s, ph);
+}
+
+// Ranks above 64 (the kernels' register budget) run as column chunks of at
+// most 64: each chunk's factor columns are gathered contiguous (pitched
+// copies), contracted, and scattered into the output columns. Columns of an
+// MTTKRP are independent, so the result is the same contraction.
+static void mttkrp_enqueue(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
+                           int order, double* dout, cudaStream_t s, Phases* ph) {
+    if (C <= 64) {
+        mttkrp_enqueue_core(t, ctx, dU, C, mode, algo, order, dout, s, ph);
+        return;
+    }
+    const int N = static_cast<int>(t.dims.size());
+    const int nch = (C + 63) / 64;
+    const int w = (C + nch - 1) / nch;
+    long long tot = 0;
+    for (int k = 0; k < N; ++k) tot += t.pdims[k] * w;
+    ctx.chunk_fac.ensure(static_cast<size_t>(tot));
+    const long long rows = t.dims[mode];
+    ctx.chunk_out.ensure(static_cast<size_t>(rows * w));
+    for (int c0 = 0; c0 < C; c0 += w) {
+        const int wc = std::min(w, C - c0);
+        std::vector<const double*> f(N);
+        long long off = 0;
+        for (int k = 0; k < N; ++k) {
+            CK(cudaMemcpy2DAsync(ctx.chunk_fac.p + off, wc * sizeof(double), dU[k] + c0, C * sizeof(double),
+                                 wc * sizeof(double), static_cast<size_t>(t.pdims[k]), cudaMemcpyDeviceToDevice, s));
+            f[k] = ctx.chunk_fac.p + off;
+            off += t.pdims[k] * wc;
+        }
+        mttkrp_enqueue_core(t, ctx, f.data(), wc, mode, algo, order, ctx.chunk_out.p, s, ph);
+        CK(cudaMemcpy2DAsync(dout + c0, C * sizeof(double), ctx.chunk_out.p, wc * sizeof(double), wc * sizeof(double),
+                             static_cast<size_t>(rows), cudaMemcpyDeviceToDevice, s));
+    }
 }
 
 static void fill_times(Context& ctx, int algo, int mode, int N, dmtk_gpu_times* tm, double wall) {

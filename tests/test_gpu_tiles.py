@@ -90,3 +90,12 @@ def test_odd_extents_wrapped_device_memory():
             torch.cuda.synchronize()
             want = ref(x, dims, f, mode)
             assert np.linalg.norm(out.cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want), (spec, mode)
+
+
+def test_ranks_above_64_column_chunks():
+    """Ranks above the kernels' 64-column budget run as independent column
+    chunks (the reference has no rank limit)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), "6x8x10:70", "9x11x13:100",
+                        "16x18x20:128", "15x7x9x5:65"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)

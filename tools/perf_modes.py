@@ -22,6 +22,7 @@ CONFIGS = {
     "64c32": ((64, 64, 64, 64, 64), 32),
     "fmri20": ((100, 100, 1200, 80), 20),
     "odd25": ((999, 1001, 997), 25),
+    "1000c100": ((1000, 1000, 1000), 100),
 }
 ALGOS = {"auto": (A.automatic, O.automatic), "one": (A.one_step, O.automatic), "left": (A.two_step, O.left),
          "right": (A.two_step, O.right), "base": (A.baseline, O.automatic)}
