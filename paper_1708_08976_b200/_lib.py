@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdmtk_gpu.so")
+# DMTK_GPU_LIB: developer override (A/B builds of the same sources)
+LIB_PATH = os.environ.get("DMTK_GPU_LIB") or os.path.join(HERE, "libdmtk_gpu.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
