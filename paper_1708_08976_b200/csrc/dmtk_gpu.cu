@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -187,6 +188,8 @@ struct PlanKey {
     bool operator<(const PlanKey& o) const { return std::tie(mode, kind, C) < std::tie(o.mode, o.kind, o.C); }
 };
 
+struct PlanCacheEntry;  // a finished ModePlan (+ boundary split) per routing key
+
 struct CsrPlan {
     long long rows = 0;
     DevBufLL rowptr, slots;
@@ -209,6 +212,11 @@ struct dmtk_gpu_tensor_s {
     bool owned = false;
     std::mutex mu;
     std::map<dmtkg::PlanKey, std::unique_ptr<dmtkg::CsrPlan>> csr;
+    // host-side plan and tensor-map caches: repeated calls on one tensor skip
+    // the tiling search and cuTensorMapEncodeTiled (small tensors are
+    // launch-bound); keyed by (mode, algorithm, order, rank) and CSR key
+    std::map<long long, std::unique_ptr<dmtkg::PlanCacheEntry>> plans;
+    std::map<std::array<long long, 7>, CUtensorMap> maps;  // (kind, L, I, R, BK, BI, BJ)
 };
 
 namespace dmtkg {
@@ -268,6 +276,11 @@ struct ModePlan {
     TcPlan tc{};
     long long n_jc = 1, jchunk = 1;  // generic
     long long ws_doubles = 0;
+};
+
+struct PlanCacheEntry {
+    ModePlan mp;
+    int best_s = 0;
 };
 
 static bool tail_of(int C, int& nb, int& tail) {
@@ -705,10 +718,16 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
                          mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
                          mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost, mp.tc.ldgsts);
         CUtensorMap map;
-        if (mp.tc.ldgsts)
+        if (mp.tc.ldgsts) {
             std::memset(&map, 0, sizeof(map));
-        else
+        } else if (X == t.d) {  // the tensor itself: one encode per view
+            const std::array<long long, 7> mkey{mp.kind, mp.L, mp.I, mp.R, mp.tc.BK, mp.tc.BI, mp.tc.BJ};
+            auto mit = t.maps.find(mkey);
+            if (mit == t.maps.end()) mit = t.maps.emplace(mkey, make_map(X, mp)).first;
+            map = mit->second;
+        } else {
             map = make_map(X, mp);
+        }
         if (!launch_mttkrp_tc(mp.tc, map, mp.nb, mp.tail, mp.kind != kTcM, mp.grid, s))
             fail(DMTK_GPU_ERUNTIME, "no tensor-core instantiation for this rank");
         check_launch("mttkrp_tc");
@@ -781,23 +800,34 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
             // re-collapsed view when a short extent would leave tile rows empty
             const bool m0 = mode == 0;
             kind = m0 ? kTcM : kTcKJ;
-            pre = plan_mode(dims, mode, C, kind, ctx.sms);
             have_pre = true;
             int best_s = 0;
-            static const bool no_swap = std::getenv("DMTK_GPU_NO_SWAP") != nullptr;
-            if (pre.kind != kGeneric && !no_swap) {
-                for (int sp = 1; sp <= N - 2; ++sp) {
-                    ModePlan cand = m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM, 1,
-                                                   ctx.sms)
-                                       : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C, kTcKJ, 1,
-                                                   ctx.sms);
-                    if (cand.kind != kGeneric && cand.cost < pre.cost * 0.97) {
-                        pre = cand;
-                        best_s = sp;
+            const long long pkey = ((static_cast<long long>(mode) * 8 + algo) * 8 + order) * 4096 + C;
+            auto pit = t.plans.find(pkey);
+            if (pit != t.plans.end()) {
+                pre = pit->second->mp;
+                best_s = pit->second->best_s;
+            } else {
+                pre = plan_mode(dims, mode, C, kind, ctx.sms);
+                static const bool no_swap = std::getenv("DMTK_GPU_NO_SWAP") != nullptr;
+                if (pre.kind != kGeneric && !no_swap) {
+                    for (int sp = 1; sp <= N - 2; ++sp) {
+                        ModePlan cand = m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM,
+                                                       1, ctx.sms)
+                                           : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C,
+                                                       kTcKJ, 1, ctx.sms);
+                        if (cand.kind != kGeneric && cand.cost < pre.cost * 0.97) {
+                            pre = cand;
+                            best_s = sp;
+                        }
                     }
                 }
+                pre.variant = best_s;
+                auto e = std::make_unique<PlanCacheEntry>();
+                e->mp = pre;
+                e->best_s = best_s;
+                t.plans[pkey] = std::move(e);
             }
-            pre.variant = best_s;
             if (best_s == 0) {
                 bgen = m0 ? make_gen(dims, 1, N, dU, C, ones) : make_gen(dims, 0, mode, dU, C, ones);
                 sgen = m0 ? make_gen(dims, 0, 0, dU, C, ones) : make_gen(dims, N, N, dU, C, ones);
@@ -846,7 +876,21 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
         }
     }
 
-    ModePlan mp = have_pre ? pre : plan_mode(vdims, vmode, C, kind, ctx.sms);
+    ModePlan mp;
+    if (have_pre) {
+        mp = pre;
+    } else {
+        const long long pkey = ((static_cast<long long>(mode) * 8 + algo) * 8 + order) * 4096 + C;
+        auto pit = t.plans.find(pkey);
+        if (pit != t.plans.end()) {
+            mp = pit->second->mp;
+        } else {
+            mp = plan_mode(vdims, vmode, C, kind, ctx.sms);
+            auto e = std::make_unique<PlanCacheEntry>();
+            e->mp = mp;
+            t.plans[pkey] = std::move(e);
+        }
+    }
     if (mode == 0) mp.out_rows = std::min(mp.out_rows, t.dims[0]);  // drop a pad row
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
     enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0),
