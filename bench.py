@@ -95,6 +95,18 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi takes a while to start: wait for its first row so that the
+        # timed region that follows is sampled from its beginning
+        t_end = time.time() + 3.0
+        while time.time() < t_end:
+            try:
+                with open(self.path) as f:
+                    if f.readline().strip():
+                        break
+            except OSError:
+                pass
+            time.sleep(0.005)
 
     def stop(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
@@ -292,7 +304,7 @@ def main():
 
     # ------------------------------------------------------------- e2e leg
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
         hx.copy_(x)
         hf = [f.cpu().numpy() for f in fs]
@@ -316,19 +328,31 @@ def main():
                                          host_out[m].ctypes.data_as(_lib.dp), None)
                 assert rc == 0, lib.dmtk_gpu_last_error()
             lib.dmtk_gpu_tensor_free(h)
+            if world > 1:  # sum the partial results of the last-mode shards
+                for m in range(N - 1):
+                    part = torch.from_numpy(host_out[m]).to(dev)
+                    dist.all_reduce(part)
+                    host_out[m][:] = part.cpu().numpy()
 
         e2e_step()  # warm-up (allocations, plans)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / args.e2e_steps
-        e2e = {"value": round(8.0 * n * N / dt / 1e9, 3), "unit": "GB/s",
+        if world > 1:  # the slowest rank sets the job's time
+            dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
+            dt = float(dtt.item())
+        e2e = {"value": round(8.0 * n * N * world / dt / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(8 * n + sum(d * C * 8 for d in dims) * N),
                "d2h_bytes_per_step": int(sum(d * C * 8 for d in dims)),
                "ms_per_step": round(dt * 1e3, 2), "steps": args.e2e_steps,
-               "path": "dmtk_gpu_tensor_upload + dmtk_gpu_mttkrp per mode (host buffers, pinned tensor)"}
+               "path": "dmtk_gpu_tensor_upload + dmtk_gpu_mttkrp per mode (host buffers, pinned tensor)"
+                       + ("; partials all-reduced over NCCL, max over ranks" if world > 1 else "")}
         del hx
 
     # ---------------------------------------------------- CPU baseline leg
