@@ -19,6 +19,8 @@
  *   DMTK_GPU_ERANGE         std::out_of_range     (mode out of range)
  *   DMTK_GPU_EOVERFLOW      std::overflow_error   (shape.cpp:20-22)
  *   DMTK_GPU_ERUNTIME       std::runtime_error    (CUDA error, no device)
+ *   DMTK_GPU_EIO            dmtk::TensorFileError (tensor_io.hpp; same
+ *                           messages as read_tensor, tensor_io.cpp:79-130)
  * There is no CPU fallback: without a usable B200 every compute call fails
  * with DMTK_GPU_ERUNTIME.
  *
@@ -39,7 +41,8 @@ enum {
     DMTK_GPU_EINVAL = 1,
     DMTK_GPU_ERANGE = 2,
     DMTK_GPU_EOVERFLOW = 3,
-    DMTK_GPU_ERUNTIME = 4
+    DMTK_GPU_ERUNTIME = 4,
+    DMTK_GPU_EIO = 5
 };
 
 /* MttkrpAlgo (mttkrp.hpp:16-21) and TwoStepOrder (mttkrp.hpp:23-27). */
@@ -69,6 +72,15 @@ int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double
 int dmtk_gpu_tensor_free(dmtk_gpu_tensor t);
 /* Shape-only view of a tensor handle (read back the device pointer). */
 int dmtk_gpu_tensor_info(dmtk_gpu_tensor t, int* ndim, int64_t* dims_out8, const double** device_ptr);
+
+/* Tensor ingest: dmtk::read_tensor (tensor_io.hpp:25) straight
+ * into HBM. Reads a DNT1 file ("DNT1", u32 version 1, u32 N, N u64 extents,
+ * the little-endian FP64 payload in natural order, nothing after it) with the
+ * reference's validation and messages, streaming the payload through two
+ * pinned staging buffers so file reads overlap the host-to-device copies. */
+int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out);
+/* The tensor's values back to host memory in natural order (total doubles). */
+int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out);
 
 /* dmtk::mttkrp (mttkrp.hpp:45) and mttkrp_baseline/one_step/two_step
  * (mttkrp.hpp:47-49) selected by `algo`. factors[k] is the host row-major

@@ -8,7 +8,7 @@
 //
 // Status codes (shared with include/dmtk_gpu.h):
 //   0 ok, 1 std::invalid_argument, 2 std::out_of_range, 3 std::overflow_error,
-//   4 any other exception. The message is kept in a thread-local buffer.
+//   4 any other exception, 5 dmtk::TensorFileError. The message is kept in a thread-local buffer.
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -24,6 +24,7 @@
 #include "dmtk/mttkrp.hpp"
 #include "dmtk/oracle.hpp"
 #include "dmtk/tensor.hpp"
+#include "dmtk/tensor_io.hpp"
 
 namespace {
 
@@ -43,6 +44,9 @@ int guarded(F&& f) {
     } catch (const std::overflow_error& e) {
         g_err = e.what();
         return 3;
+    } catch (const dmtk::TensorFileError& e) {
+        g_err = e.what();
+        return 5;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 4;
@@ -76,6 +80,29 @@ void put_times(const dmtk::TimeBreakdown& t, double* out8) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// dmtk::write_tensor / read_tensor (tensor_io.hpp:24-25).
+int ref_write_tensor(const char* path, int ndim, const int64_t* dims, const double* x) {
+    return guarded([&] {
+        const dmtk::Shape shape = shape_of(ndim, dims);
+        const dmtk::DenseTensor t = dmtk::DenseTensor::borrow(shape, x, shape.total());
+        dmtk::write_tensor(path, t);
+    });
+}
+
+// values_out may be NULL (validation only); capacity in doubles.
+int ref_read_tensor(const char* path, int* ndim, int64_t* dims_out64, double* values_out, int64_t capacity) {
+    return guarded([&] {
+        const dmtk::DenseTensor t = dmtk::read_tensor(path);
+        *ndim = static_cast<int>(t.shape().ndim());
+        for (int k = 0; k < *ndim; ++k) dims_out64[k] = t.shape().dim(k);
+        if (values_out) {
+            const auto v = t.values();
+            if (static_cast<int64_t>(v.size()) > capacity) throw std::invalid_argument("capacity");
+            std::memcpy(values_out, v.data(), v.size() * sizeof(double));
+        }
+    });
+}
 
 // dmtk::mttkrp (mttkrp.hpp:45). algo: 0 baseline, 1 one_step, 2 two_step,
 // 3 automatic (mttkrp.hpp:16-21); order: 0 automatic, 1 left, 2 right.

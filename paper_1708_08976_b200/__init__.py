@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     MttkrpResult,
     OutOfRange,
     ShapeOverflow,
+    TensorFileError,
     TwoStepOrder,
     choose_order,
     cp_als,

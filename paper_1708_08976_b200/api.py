@@ -16,6 +16,7 @@ Layouts are the reference's: tensors in natural order (mode 0 fastest, i.e.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -42,7 +43,11 @@ class DeviceError(RuntimeError):
     pass
 
 
-_ERR = {1: InvalidArgument, 2: OutOfRange, 3: ShapeOverflow, 4: DeviceError}
+class TensorFileError(RuntimeError):
+    """dmtk::TensorFileError (tensor_io.hpp)."""
+
+
+_ERR = {1: InvalidArgument, 2: OutOfRange, 3: ShapeOverflow, 4: DeviceError, 5: TensorFileError}
 
 
 def _check(rc: int) -> None:
@@ -106,6 +111,24 @@ class DenseTensor:
                                         C.byref(t._handle)))
         t._owner = owner
         return t
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "DenseTensor":
+        """dmtk::read_tensor (tensor_io.hpp:25) straight into HBM (DNT1 file)."""
+        h = C.c_void_p()
+        _check(lib.dmtk_gpu_tensor_load(device, os.fsencode(path), C.byref(h)))
+        with open(path, "rb") as f:  # the header the library just validated
+            n = int(np.frombuffer(f.read(12)[8:], dtype="<u4")[0])
+            dims = tuple(int(v) for v in np.frombuffer(f.read(8 * n), dtype="<u8"))
+        t = cls(dims, None, device)
+        t._handle = h
+        return t
+
+    def download(self) -> np.ndarray:
+        """The values in natural order, from the device copy."""
+        out = np.empty(self.total)
+        _check(lib.dmtk_gpu_tensor_download(self.handle(), _dp(out)))
+        return out
 
     @property
     def ndim(self) -> int:

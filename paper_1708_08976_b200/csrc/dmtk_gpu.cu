@@ -4,11 +4,16 @@
 // on-device CP-ALS loop. Kernels live in mttkrp_tc*.cu and kernels.cu.
 #include <cudaTypedefs.h>
 
+#include <sys/stat.h>
+#include <unistd.h>
+#include <thread>
 #include <algorithm>
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -1150,6 +1155,168 @@ int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double
         t->d = device_ptr;
         t->owned = false;
         *out = t.release();
+    });
+}
+
+// ---------------------------------------------------------- tensor ingest
+// dmtk::read_tensor (tensor_io.cpp:79-130) into HBM: the same checks in the
+// same order with the same messages; the payload streams through two pinned
+// staging buffers (file read of one chunk overlaps the H2D copy of the other).
+namespace dmtkg {
+static void read_exact(std::FILE* f, void* dst, size_t count, uint64_t offset, const char* what) {
+    const size_t got = std::fread(dst, 1, count, f);
+    if (got != count)
+        fail(DMTK_GPU_EIO, std::string("tensor file truncated reading ") + what + ": expected " +
+                               std::to_string(count) + " bytes at offset " + std::to_string(offset) + ", got " +
+                               std::to_string(got));
+}
+}  // namespace dmtkg
+
+int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        if (!path || !out) fail(DMTK_GPU_EINVAL, "tensor_load: null argument");
+        std::FILE* f = std::fopen(path, "rb");
+        if (!f) fail(DMTK_GPU_EIO, std::string("cannot open '") + path + "' for reading");
+        struct Closer {
+            std::FILE* f;
+            ~Closer() { std::fclose(f); }
+        } closer{f};
+        static_assert(sizeof(double) == 8, "FP64 payload");
+        char magic[4];
+        read_exact(f, magic, 4, 0, "magic");
+        if (std::memcmp(magic, "DNT1", 4) != 0)
+            fail(DMTK_GPU_EIO, std::string("'") + path + "' is not a tensor file: bad magic at offset 0");
+        uint32_t version = 0, n = 0;  // little-endian host (x86-64 / aarch64)
+        read_exact(f, &version, 4, 4, "version");
+        if (version != 1)
+            fail(DMTK_GPU_EIO, "unsupported tensor file version " + std::to_string(version) + " (expected 1)");
+        read_exact(f, &n, 4, 8, "mode count");
+        if (n < 1 || n > 64) fail(DMTK_GPU_EIO, "tensor file declares " + std::to_string(n) + " modes");
+        std::vector<int64_t> dims(n);
+        uint64_t offset = 12;
+        for (uint32_t i = 0; i < n; ++i) {
+            uint64_t ext = 0;
+            read_exact(f, &ext, 8, offset, "extent");
+            if (ext < 1 || ext > static_cast<uint64_t>(INT64_MAX))
+                fail(DMTK_GPU_EIO,
+                     "tensor file declares extent " + std::to_string(ext) + " for mode " + std::to_string(i));
+            dims[i] = static_cast<int64_t>(ext);
+            offset += 8;
+        }
+        auto d = checked_dims(static_cast<int>(n), dims.data());  // Shape(dims): overflow check
+        if (static_cast<int>(n) > kMaxFactors + 1) fail(DMTK_GPU_EINVAL, "dmtk_gpu: tensor order above 13 unsupported");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        auto t = std::make_unique<dmtk_gpu_tensor_s>();
+        t->device = device;
+        t->dims = d;
+        t->total = prod(d, 0, static_cast<int>(n));
+        t->pdims = d;
+        if (d[0] % 2 != 0) t->pdims[0] = d[0] + 1;  // same padded layout as dmtk_gpu_tensor_upload
+        t->ptotal = prod(t->pdims, 0, static_cast<int>(n));
+        double* p = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(t->ptotal) * sizeof(double), ctx.stream));
+        t->d = p;
+        t->owned = true;
+        // chunks of whole mode-0 runs (the padded copy is pitched per run)
+        const long long run = d[0];
+        const long long runs = t->total / run;
+        const long long chunk_runs = std::max<long long>(1, (64LL << 20) / (run * 8));
+        const size_t chunk_bytes = static_cast<size_t>(chunk_runs * run * 8);
+        double* stage[2] = {nullptr, nullptr};
+        cudaEvent_t done[2];
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&stage[0]), chunk_bytes, cudaHostAllocDefault));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&stage[1]), chunk_bytes, cudaHostAllocDefault));
+        CK(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+        struct Cleanup {
+            double** st;
+            cudaEvent_t* ev;
+            cudaStream_t s;
+            ~Cleanup() {
+                cudaStreamSynchronize(s);
+                cudaFreeHost(st[0]);
+                cudaFreeHost(st[1]);
+                cudaEventDestroy(ev[0]);
+                cudaEventDestroy(ev[1]);
+            }
+        } cleanup{stage, done, ctx.stream};
+        const size_t pitch = static_cast<size_t>(t->pdims[0]) * sizeof(double);
+        // the reference reads the payload in one piece: same truncation message
+        // (bytes available after the header) before any chunk is read
+        struct stat st {};
+        if (fstat(fileno(f), &st) != 0) fail(DMTK_GPU_EIO, std::string("cannot stat '") + path + "'");
+        const uint64_t payload = static_cast<uint64_t>(t->total) * 8;
+        const uint64_t avail = static_cast<uint64_t>(st.st_size) > offset ? static_cast<uint64_t>(st.st_size) - offset : 0;
+        if (avail < payload)
+            fail(DMTK_GPU_EIO, "tensor file truncated reading payload: expected " + std::to_string(payload) +
+                                   " bytes at offset " + std::to_string(offset) + ", got " + std::to_string(avail));
+        // each chunk is read by several threads (parallel page-cache copies)
+        const int fd = fileno(f);
+        auto pread_all = [&](char* dst, size_t count, uint64_t at) {
+            const int nt = count >= (8u << 20) ? 8 : 1;
+            std::vector<std::thread> th;
+            std::atomic<bool> bad{false};
+            const size_t part = (count + nt - 1) / nt;
+            for (int k = 0; k < nt; ++k) {
+                const size_t b0 = std::min(count, part * k), b1 = std::min(count, part * (k + 1));
+                th.emplace_back([&, b0, b1] {
+                    size_t done_ = b0;
+                    while (done_ < b1) {
+                        const ssize_t r = pread(fd, dst + done_, b1 - done_, static_cast<off_t>(at + done_));
+                        if (r <= 0) {
+                            bad = true;
+                            return;
+                        }
+                        done_ += static_cast<size_t>(r);
+                    }
+                });
+            }
+            for (auto& x : th) x.join();
+            if (bad) fail(DMTK_GPU_EIO, std::string("read of '") + path + "' failed");
+        };
+        long long r0 = 0;
+        for (int b = 0; r0 < runs; b ^= 1) {
+            const long long nr = std::min(chunk_runs, runs - r0);
+            CK(cudaEventSynchronize(done[b]));  // this staging buffer's previous copy has finished
+            pread_all(reinterpret_cast<char*>(stage[b]), static_cast<size_t>(nr * run * 8), offset);
+            if (t->pdims == t->dims) {
+                CK(cudaMemcpyAsync(p + r0 * run, stage[b], static_cast<size_t>(nr * run * 8), cudaMemcpyHostToDevice,
+                                   ctx.stream));
+            } else {
+                CK(cudaMemcpy2DAsync(p + r0 * t->pdims[0], pitch, stage[b], static_cast<size_t>(run) * 8,
+                                     static_cast<size_t>(run) * 8, static_cast<size_t>(nr), cudaMemcpyHostToDevice,
+                                     ctx.stream));
+                CK(cudaMemset2DAsync(p + r0 * t->pdims[0] + run, pitch, 0, sizeof(double), static_cast<size_t>(nr),
+                                     ctx.stream));
+            }
+            CK(cudaEventRecord(done[b], ctx.stream));
+            offset += static_cast<uint64_t>(nr * run * 8);
+            r0 += nr;
+        }
+        if (static_cast<uint64_t>(st.st_size) > offset)
+            fail(DMTK_GPU_EIO, "tensor file has trailing bytes after offset " + std::to_string(offset));
+        CK(cudaStreamSynchronize(ctx.stream));
+        *out = t.release();
+    });
+}
+
+int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out) {
+    return guarded([&] {
+        if (!t || !host_out) fail(DMTK_GPU_EINVAL, "tensor_download: null argument");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        if (t->pdims == t->dims) {
+            CK(cudaMemcpyAsync(host_out, t->d, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx.stream));
+        } else {
+            CK(cudaMemcpy2DAsync(host_out, static_cast<size_t>(t->dims[0]) * 8, t->d,
+                                 static_cast<size_t>(t->pdims[0]) * 8, static_cast<size_t>(t->dims[0]) * 8,
+                                 static_cast<size_t>(t->total / t->dims[0]), cudaMemcpyDeviceToHost, ctx.stream));
+        }
+        CK(cudaStreamSynchronize(ctx.stream));
     });
 }
 

@@ -196,11 +196,27 @@ class Ref:
                                  C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int), _dp]
         L.ref_fit.argtypes = [C.c_int, _ip, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]
+        L.ref_write_tensor.argtypes = [C.c_char_p, C.c_int, _ip, _dp]
+        L.ref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), _ip, _dp, C.c_int64]
         self.L = L
 
     def _check(self, rc: int):
         if rc != 0:
             raise RefError(rc, self.L.ref_last_error().decode())
+
+    def write_tensor(self, path: str, x: np.ndarray, dims) -> None:
+        """dmtk::write_tensor (tensor_io.hpp:24): a DNT1 file."""
+        d = _i64(dims)
+        self._check(self.L.ref_write_tensor(os.fsencode(path), len(d), d.ctypes.data_as(_ip), _d(x)))
+
+    def read_tensor(self, path: str, capacity: int = 0):
+        """dmtk::read_tensor (tensor_io.hpp:25): (dims, values) or RefError(5, msg)."""
+        nd = C.c_int()
+        dims = np.zeros(64, dtype=np.int64)
+        vals = np.empty(max(capacity, 1))
+        self._check(self.L.ref_read_tensor(os.fsencode(path), C.byref(nd), dims.ctypes.data_as(_ip),
+                                           _d(vals) if capacity else None, capacity))
+        return tuple(int(v) for v in dims[:nd.value]), (vals if capacity else None)
 
     def gen_tensor(self, dims, seed: int) -> np.ndarray:
         d = _i64(dims)
