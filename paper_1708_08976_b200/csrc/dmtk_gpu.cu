@@ -213,6 +213,10 @@ struct dmtk_gpu_tensor_s {
     // a zero row and mode-0 results are truncated (adding exact zeros).
     std::vector<long long> pdims;
     long long ptotal = 0;
+    // a wrapped (borrowed, immutable: tensor.hpp:11-18) buffer with an odd first
+    // extent is repacked once into a padded library-owned copy on first use
+    const double* user = nullptr;  // the caller's buffer when d is that copy
+    bool repack_failed = false;
     const double* d = nullptr;
     bool owned = false;
     std::mutex mu;
@@ -321,7 +325,7 @@ static bool tail_of(int C, int& nb, int& tail) {
 // tile of one stage; each waits on a factor-row load), so the pressure is
 // items per byte of X: b = G * 32 KB / A_BYTES (1 for RB 2 or 4 at G = 1,
 // 4/3 for RB 3). Measured on 1000^3 / 180^4 / fMRI shapes (r01 sweep):
-// b = 4/3 costs ~5%, b = 2 ~20%, b = 4 ~55%; RB 2 wins near-ties by ~1%.
+// b = 4/3 costs ~5%, b = 2 ~20%, b = 4 ~55%; RB 4 wins near-ties by 1-3%.
 struct Tiling {
     int RB, G, BI, BJ;
 };
@@ -333,7 +337,9 @@ static double kwaste(long long K, long long step) {
 static double tile_cost(int RB, int G) {
     const double a_kb = tc_bm(RB) * tc_bk(RB) * 8 / 1024.0;
     const double b = G * 32.0 / a_kb - 1.0;
-    return (1.0 + 0.15 * b + 0.08 * b * b) * (RB == 2 ? 1.0 : 1.01);
+    // taller tiles read fewer B fragments per DMMA from shared memory (less
+    // contention with the TMA and builder traffic): measured 1-3% per mode
+    return (1.0 + 0.15 * b + 0.08 * b * b) * (RB == 4 ? 1.0 : (RB == 3 ? 1.01 : 1.02));
 }
 
 static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int nb, int tail,
@@ -741,6 +747,40 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
     launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s);
     check_launch("slot_reduce");
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
+}
+
+// Borrowed tensors keep the caller's layout, but an odd first extent would
+// leave TMA unusable (8-byte cp.async producer, 0.03-0.3 of roofline): repack
+// once into the padded layout of dmtk_gpu_tensor_upload (one pitched D2D
+// copy; the borrowed buffer must stay unchanged while wrapped, as the
+// reference's DenseTensor::borrow requires). Falls back to the cp.async
+// producer when the copy cannot be allocated.
+static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
+    if (t.owned || t.user || t.repack_failed || t.dims[0] % 2 == 0 || t.total == 0) return;
+    std::vector<long long> pd = t.dims;
+    pd[0] += 1;
+    const long long pt = prod(pd, 0, static_cast<int>(pd.size()));
+    double* p = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(pt) * sizeof(double), ctx.stream) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        t.repack_failed = true;
+        return;
+    }
+    const size_t rows = static_cast<size_t>(t.total / t.dims[0]);
+    const size_t pitch = static_cast<size_t>(pd[0]) * sizeof(double);
+    CK(cudaStreamSynchronize(s));  // the borrowed data is final at this call
+    CK(cudaMemcpy2DAsync(p, pitch, t.d, static_cast<size_t>(t.dims[0]) * sizeof(double),
+                         static_cast<size_t>(t.dims[0]) * sizeof(double), rows, cudaMemcpyDeviceToDevice, ctx.stream));
+    CK(cudaMemset2DAsync(p + t.dims[0], pitch, 0, sizeof(double), rows, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    t.user = t.d;
+    t.d = p;
+    t.pdims = pd;
+    t.ptotal = pt;
+    t.csr.clear();
+    t.plans.clear();
+    t.maps.clear();
 }
 
 static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
@@ -1323,7 +1363,7 @@ int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out) {
 int dmtk_gpu_tensor_free(dmtk_gpu_tensor t) {
     return guarded([&] {
         if (!t) return;
-        if (t->owned && t->d) {
+        if ((t->owned || t->user) && t->d) {  // own allocation, or the padded copy of a borrowed buffer
             Context& ctx = context(t->device);
             cudaSetDevice(t->device);
             cudaFreeAsync(const_cast<double*>(t->d), ctx.stream);
@@ -1339,7 +1379,7 @@ int dmtk_gpu_tensor_info(dmtk_gpu_tensor t, int* ndim, int64_t* dims_out8, const
         if (ndim) *ndim = static_cast<int>(t->dims.size());
         if (dims_out8)
             for (size_t k = 0; k < t->dims.size() && k < 8; ++k) dims_out8[k] = t->dims[k];
-        if (device_ptr) *device_ptr = t->d;
+        if (device_ptr) *device_ptr = t->user ? t->user : t->d;
     });
 }
 
@@ -1368,6 +1408,7 @@ int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factor
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
         const long long C = factor_cols[0];
+        ensure_layout(*t, ctx, ctx.stream);
         std::vector<const double*> dptr;
         upload_factors(ctx, *t, factors, C, dptr);
         const long long rows = t->dims[mode];
@@ -1399,6 +1440,7 @@ int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factor
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+        ensure_layout(*t, ctx, s);
         std::vector<const double*> f(device_factors, device_factors + N);
         if (t->pdims[0] != t->dims[0]) {  // padded tensor: first factor with a zero row
             const size_t rowsz = static_cast<size_t>(rank) * sizeof(double);
@@ -1501,6 +1543,7 @@ int dmtk_gpu_tensor_norm(dmtk_gpu_tensor t, double* out) {
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
+        ensure_layout(*t, ctx, ctx.stream);
         *out = tensor_norm_dev(*t, ctx);
     });
 }
@@ -1575,6 +1618,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         CK(cudaSetDevice(t->device));
         cudaStream_t s = ctx.stream;
 
+        ensure_layout(*t, ctx, s);
         // KruskalModel::random (cp_als.cpp:87-99): one mt19937_64 stream
         std::mt19937_64 rng(cfg->seed);
         long long ftot = 0, maxrows = 0, ptot = 0;  // logical / physical (padded first factor) sizes
@@ -1824,6 +1868,7 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
+        ensure_layout(*t, ctx, ctx.stream);
         const double normx = tensor_norm_dev(*t, ctx);
         std::vector<const double*> dptr;
         upload_factors(ctx, *t, factors, C, dptr);

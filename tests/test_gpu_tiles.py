@@ -63,8 +63,8 @@ def test_odd_extents_uploaded():
 
 
 def test_odd_extents_wrapped_device_memory():
-    """Device-resident tensors keep the caller's layout: odd strides take the
-    8-byte cp.async producer instead of TMA."""
+    """Borrowed device buffers with an odd first extent are repacked once into
+    the padded layout on first use."""
     import numpy as np
     import torch
 
@@ -99,3 +99,43 @@ def test_ranks_above_64_column_chunks():
                         "16x18x20:128", "15x7x9x5:65"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+
+
+def test_cp_async_producer_forced():
+    """The 8-byte cp.async producer (TMA-incompatible strides or base) on every
+    flavor and tile shape, forced through DMTK_GPU_FORCE_LDGSTS."""
+    for rb in (2, 3, 4):
+        env = dict(os.environ, DMTK_GPU_FORCE_LDGSTS="1", DMTK_GPU_FORCE_RB=str(rb))
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), "10x12x14:20",
+                            "16x18x20:25", "40x40x12x8:20", "9x11x13:3", "130x66x34:9"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert "failures: 0" in r.stdout, (rb, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l))
+
+
+def test_misaligned_borrowed_base():
+    """A borrowed buffer whose base is only 8-byte aligned (TMA needs 16) runs
+    through the cp.async producer."""
+    import numpy as np
+    import torch
+
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200 import MttkrpAlgo as A, TwoStepOrder as O
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from check_shapes import ref
+
+    rng = np.random.default_rng(5)
+    dims, C = (20, 18, 16), 9
+    x = rng.uniform(-1, 1, int(np.prod(dims)))
+    f = [rng.uniform(-1, 1, (d, C)) for d in dims]
+    buf = torch.zeros(x.size + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(x).cuda()
+    t = dg.DenseTensor.from_device(dims, buf.data_ptr() + 8, owner=buf)
+    fd = [torch.from_numpy(u).cuda() for u in f]
+    for mode in range(3):
+        out = torch.empty((dims[mode], C), dtype=torch.float64, device="cuda")
+        dg.mttkrp_device(t, [u.data_ptr() for u in fd], C, mode, A.automatic, O.automatic, out.data_ptr(),
+                         torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        want = ref(x, dims, f, mode)
+        assert np.linalg.norm(out.cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want), mode
