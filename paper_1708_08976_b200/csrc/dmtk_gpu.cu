@@ -290,6 +290,7 @@ struct ModePlan {
 struct PlanCacheEntry {
     ModePlan mp;
     int best_s = 0;
+    int ord = 0;  // two_step with automatic order: the order chosen
 };
 
 static bool tail_of(int C, int& nb, int& tail) {
@@ -904,8 +905,27 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
         }
     } else {  // two_step (interior only; validated by the caller)
         int ord = order;
-        if (ord == DMTK_GPU_ORDER_AUTOMATIC)
-            ord = prod(dims, 0, mode) > prod(dims, mode + 1, N) ? DMTK_GPU_ORDER_LEFT : DMTK_GPU_ORDER_RIGHT;
+        if (ord == DMTK_GPU_ORDER_AUTOMATIC) {
+            // The reference picks the order by the larger partial (choose_order,
+            // mttkrp.cpp:246-248), a CPU cost rule; the order does not change
+            // the result beyond rounding, so the GPU compares its own modelled
+            // costs of the two views instead (K-major tiles measure 5-10% slower
+            // than M-major ones at equal padding).
+            const long long pkey = ((static_cast<long long>(mode) * 8 + algo) * 8 + order) * 4096 + C;
+            auto pit = t.plans.find(pkey);
+            if (pit != t.plans.end()) {
+                ord = pit->second->ord;
+            } else {
+                const ModePlan pr = plan_mode(dims, mode, C, kTcM, ctx.sms);
+                const ModePlan pl = plan_mode(dims, mode, C, kTcKJ, ctx.sms);
+                const bool left = pl.kind != kGeneric && (pr.kind == kGeneric || pl.cost * 1.06 < pr.cost);
+                ord = left ? DMTK_GPU_ORDER_LEFT : DMTK_GPU_ORDER_RIGHT;
+                auto e = std::make_unique<PlanCacheEntry>();
+                e->mp = left ? pl : pr;
+                e->ord = ord;
+                t.plans[pkey] = std::move(e);
+            }
+        }
         if (ord == DMTK_GPU_ORDER_RIGHT) {
             kind = kTcM;
             bgen = make_gen(dims, mode + 1, N, dU, C, ones);
