@@ -811,11 +811,9 @@ void launch_solve_psd_inverse(const double* H, int n, const double* M, long long
     double* V = scratch + 64 * 64;
     double* gain = V + 64 * 64;
     const int sm2 = 2 * n * n * 8;
-    static int opted = 0;
-    if (!opted) {
+    static std::atomic<unsigned long long> opted{0};
+    if (first_on_device(opted))
         cudaFuncSetAttribute(cholesky_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
-        opted = 1;
-    }
     cholesky_inverse_kernel<<<1, 32, sm2, s>>>(H, n, Hinv, flag);
     const long long tot = rows * n;
     apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, n * n * 8, s>>>(Hinv, n, M, rows, U, flag);

@@ -3,9 +3,20 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "mttkrp_plan.h"
 
 namespace dmtkg {
+
+// Function attributes (the shared-memory opt-in) belong to the current
+// device's context: raise them once per device, outside any graph capture.
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
+}
 
 void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
                       cudaStream_t s);

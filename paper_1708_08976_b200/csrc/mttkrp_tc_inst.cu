@@ -24,11 +24,8 @@ template <int TAIL, bool KM>
 static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaStream_t s) {
     if constexpr (tc_has_tail(TAIL)) {
         auto k = mttkrp_tc_kernel<TC_NB, TAIL, KM, TC_RB>;
-        static int opted = 0;  // raise the opt-in once (not a stream op: stays out of graph captures)
-        if (p.smem > opted) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            opted = 227 * 1024;
-        }
+        static std::atomic<unsigned long long> opted{0};  // per device; not a stream op (graph-safe)
+        if (first_on_device(opted)) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         k<<<grid, tc_threads(TC_RB), p.smem, s>>>(map, p);
     }
 }
