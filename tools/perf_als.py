@@ -36,7 +36,14 @@ def main():
     ap.add_argument("--tree", action="store_true", help="dimension-tree sweep (two tensor passes per iteration)")
     args = ap.parse_args()
     dims = tuple(int(d) for d in args.dims.split(","))
-    x = fmri_tensor(dims)
+    if len(dims) == 4:
+        x = fmri_tensor(dims)
+    else:  # other shapes: seeded U[0,1)
+        g = torch.Generator(device="cuda").manual_seed(1)
+        n = 1
+        for d in dims:
+            n *= d
+        x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
     t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
     dg.cp_als(t, dg.AlsConfig(rank=args.rank, max_iters=2, tol=0.0, seed=1, dimension_tree=args.tree))  # warm-up
     torch.cuda.synchronize()
