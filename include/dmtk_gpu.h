@@ -79,6 +79,15 @@ int dmtk_gpu_tensor_info(dmtk_gpu_tensor t, int* ndim, int64_t* dims_out8, const
  * reference's validation and messages, streaming the payload through two
  * pinned staging buffers so file reads overlap the host-to-device copies. */
 int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out);
+/* Tensors symmetric in modes 0 and 1 (BASELINE config 5's fMRI slices;
+ * SURVEY 8f-4): checks X(i, j, ...) == X(j, i, ...) exactly (EINVAL
+ * otherwise) and returns a new handle holding only the upper triangle of
+ * every slice (I (I + 1) / 2 pairs instead of I^2 entries). Such a handle
+ * supports dmtk_gpu_cp_als -- a dimension-tree sweep whose left half is the
+ * pair index, so both tensor passes read about half the bytes; fits agree with
+ * the reference's CP-ALS on the full tensor -- and dmtk_gpu_tensor_norm (of the
+ * full tensor); the other calls reject it. */
+int dmtk_gpu_tensor_pack_sym01(dmtk_gpu_tensor t, dmtk_gpu_tensor* out);
 /* The tensor's values back to host memory in natural order (total doubles). */
 int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out);
 

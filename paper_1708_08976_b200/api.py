@@ -124,6 +124,17 @@ class DenseTensor:
         t._handle = h
         return t
 
+    def pack_symmetric01(self) -> "DenseTensor":
+        """A packed copy of a tensor symmetric in modes 0 and 1 (upper triangle
+        of every slice; dmtk_gpu_tensor_pack_sym01). Supports cp_als (a
+        dimension-tree sweep reading about half the bytes) and tensor_norm."""
+        h = C.c_void_p()
+        _check(lib.dmtk_gpu_tensor_pack_sym01(self.handle(), C.byref(h)))
+        t = DenseTensor(self.dims, None, self.device)
+        t._handle = h
+        t._owner = self  # the packed copy is independent; keep the source alive anyway
+        return t
+
     def download(self) -> np.ndarray:
         """The values in natural order, from the device copy."""
         out = np.empty(self.total)

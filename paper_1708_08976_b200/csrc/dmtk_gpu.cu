@@ -217,6 +217,10 @@ struct dmtk_gpu_tensor_s {
     // extent is repacked once into a padded library-owned copy on first use
     const double* user = nullptr;  // the caller's buffer when d is that copy
     bool repack_failed = false;
+    // symmetric in modes 0 and 1, stored packed (dmtk_gpu_tensor_pack_sym01):
+    // dims stay the logical (I, I, rest...); pdims = (pairs padded, rest...)
+    bool sym01 = false;
+    double full_norm = 0.0;
     const double* d = nullptr;
     bool owned = false;
     std::mutex mu;
@@ -1362,8 +1366,50 @@ int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out) {
     });
 }
 
+int dmtk_gpu_tensor_pack_sym01(dmtk_gpu_tensor t, dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        if (!t || !out) fail(DMTK_GPU_EINVAL, "pack_sym01: null argument");
+        if (t->sym01) fail(DMTK_GPU_EINVAL, "pack_sym01: tensor is already packed");
+        const int N = static_cast<int>(t->dims.size());
+        if (N < 3 || t->dims[0] != t->dims[1])
+            fail(DMTK_GPU_EINVAL, "pack_sym01: needs an order >= 3 tensor with I_0 == I_1");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        ensure_layout(*t, ctx, ctx.stream);
+        const long long I = t->dims[0], pd0 = t->pdims[0], R = prod(t->dims, 2, N);
+        CK(cudaMemsetAsync(ctx.flag, 0, sizeof(int), ctx.stream));
+        launch_sym01_check(t->d, I, pd0, R, ctx.flag, ctx.stream);
+        check_launch("sym01_check");
+        int asym = 0;
+        CK(cudaMemcpyAsync(&asym, ctx.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+        if (asym) fail(DMTK_GPU_EINVAL, "pack_sym01: tensor is not symmetric in modes 0 and 1");
+        const double norm = tensor_norm_dev(*t, ctx);
+        auto p = std::make_unique<dmtk_gpu_tensor_s>();
+        p->device = t->device;
+        p->dims = t->dims;
+        p->total = t->total;
+        const long long P = I * (I + 1) / 2, Pp = P + (P & 1);
+        p->pdims.push_back(Pp);
+        for (int k = 2; k < N; ++k) p->pdims.push_back(t->dims[k]);
+        p->ptotal = Pp * R;
+        p->sym01 = true;
+        p->full_norm = norm;
+        double* buf = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), static_cast<size_t>(p->ptotal) * sizeof(double), ctx.stream));
+        p->d = buf;
+        p->owned = true;
+        launch_sym01_pack(t->d, I, pd0, R, Pp, buf, ctx.stream);
+        check_launch("sym01_pack");
+        CK(cudaStreamSynchronize(ctx.stream));
+        *out = p.release();
+    });
+}
+
 int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out) {
     return guarded([&] {
+        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
         if (!t || !host_out) fail(DMTK_GPU_EINVAL, "tensor_download: null argument");
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
@@ -1416,6 +1462,7 @@ int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factor
                     const int64_t* factor_cols, int64_t mode, int algo, int order, int threads, double* out,
                     dmtk_gpu_times* times) {
     return guarded([&] {
+        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
         validate_factors(t, nfactors, factors, factor_rows, factor_cols, mode, threads, "mttkrp");
         const int N = static_cast<int>(t->dims.size());
         if (algo < 0 || algo > 3) fail(DMTK_GPU_EINVAL, "mttkrp: unknown algorithm");
@@ -1449,6 +1496,7 @@ int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factor
                            int order, double* device_out, void* stream) {
     return guarded([&] {
         if (!t) fail(DMTK_GPU_EINVAL, "mttkrp: null tensor");
+        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
         const int N = static_cast<int>(t->dims.size());
         if (mode < 0 || mode >= N)
             fail(DMTK_GPU_ERANGE, "mttkrp: mode " + std::to_string(mode) + " outside [0, " + std::to_string(N) + ")");
@@ -1563,6 +1611,10 @@ int dmtk_gpu_tensor_norm(dmtk_gpu_tensor t, double* out) {
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
+        if (t->sym01) {
+            *out = t->full_norm;
+            return;
+        }
         ensure_layout(*t, ctx, ctx.stream);
         *out = tensor_norm_dev(*t, ctx);
     });
@@ -1638,25 +1690,28 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         CK(cudaSetDevice(t->device));
         cudaStream_t s = ctx.stream;
 
-        ensure_layout(*t, ctx, s);
+        if (!t->sym01) ensure_layout(*t, ctx, s);
+        // factor rows on the device: the physical extents (a padded first
+        // factor), or the logical ones for a packed symmetric tensor
+        const std::vector<long long> frows = t->sym01 ? t->dims : t->pdims;
         // KruskalModel::random (cp_als.cpp:87-99): one mt19937_64 stream
         std::mt19937_64 rng(cfg->seed);
         long long ftot = 0, maxrows = 0, ptot = 0;  // logical / physical (padded first factor) sizes
         for (int k = 0; k < N; ++k) {
             ftot += t->dims[k] * C;
-            ptot += t->pdims[k] * C;
-            maxrows = std::max(maxrows, t->pdims[k]);
+            ptot += frows[k] * C;
+            maxrows = std::max(maxrows, frows[k]);
         }
         std::vector<double> hf(static_cast<size_t>(ptot), 0.0);
         {
             long long po = 0;
             for (int k = 0; k < N; ++k) {  // reference stream order; pad rows stay zero
                 for (long long e = 0; e < t->dims[k] * C; ++e) hf[po + e] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
-                po += t->pdims[k] * C;
+                po += frows[k] * C;
             }
         }
 
-        const double normx = tensor_norm_dev(*t, ctx);
+        const double normx = t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx);
         *tensor_norm_out = normx;
         *n_iters = 0;
         *zero_tensor = 0;
@@ -1689,7 +1744,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         for (int k = 0; k < N; ++k) {
             Um[k] = F.p + off;
             Uc[k] = Um[k];
-            off += t->pdims[k] * C;
+            off += frows[k] * C;
             launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
             check_launch("gram");
         }
@@ -1745,9 +1800,10 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
                 als_upd(k, Pbuf.p);
                 return;
             }
-            const long long A = prod(t->pdims, lo, k), dt = t->pdims[k], B = prod(t->pdims, k + 1, hi);
-            const KrpGen kl = make_gen(t->pdims, lo, k, Uc.data(), C, ctx.ones.p);
-            const KrpGen kr = make_gen(t->pdims, k + 1, hi, Uc.data(), C, ctx.ones.p);
+            const std::vector<long long>& hd = t->sym01 ? t->dims : t->pdims;  // modes >= 2 are unpadded
+            const long long A = prod(hd, lo, k), dt = hd[k], B = prod(hd, k + 1, hi);
+            const KrpGen kl = make_gen(hd, lo, k, Uc.data(), C, ctx.ones.p);
+            const KrpGen kr = make_gen(hd, k + 1, hi, Uc.data(), C, ctx.ones.p);
             ctx.mttv.ensure(static_cast<size_t>(multittv_ws_doubles(A, dt, B, C)));
             launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
             count_launch(1);
@@ -1759,7 +1815,47 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             int mode;
         };
         std::vector<Step> steps;
-        if (!tree) {
+        // packed symmetric tensor (modes 0 and 1): a dimension tree whose left
+        // half {0, 1} is the packed pair index -- each pass reads the packed
+        // tensor (about half the bytes); see dmtk_gpu_tensor_pack_sym01
+        DevBuf Qb, Wb;
+        const long long sI = t->sym01 ? t->dims[0] : 0;
+        const long long sPp = t->sym01 ? t->pdims[0] : 0;
+        const long long sR = t->sym01 ? prod(t->dims, 2, N) : 0;
+        std::vector<const double*> pk_ptrs;
+        if (t->sym01) {
+            Qb.ensure(static_cast<size_t>(sPp * C));
+            Wb.ensure(static_cast<size_t>(sPp * C));
+            Pbuf.ensure(static_cast<size_t>(sR * C));
+            pk_ptrs.assign(t->pdims.size(), nullptr);
+            for (int k = 2; k < N; ++k) pk_ptrs[k - 1] = Uc[k];
+            const int Np = static_cast<int>(t->pdims.size());
+            auto sym_left = [&, Np]() {  // Q(p, c) = sum_r Xp(p, r) KR(r, c)
+                const ModePlan mp = plan_view(1, sPp, sR, C, kTcM, 0, ctx.sms);
+                const KrpGen bg = make_gen(t->pdims, 1, Np, pk_ptrs.data(), C, ctx.ones.p);
+                const KrpGen sg = make_gen(t->pdims, 0, 0, pk_ptrs.data(), C, ctx.ones.p);
+                enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, 400 * 128, -1, Qb.p, s, nullptr);
+            };
+            auto sym_mode = [&](int k) {  // mode 0 (with U_1) or mode 1 (with the new U_0)
+                launch_sym01_mttv(Qb.p, sI, C, k == 0 ? Um[1] : Um[0], M.p, s);
+                check_launch("sym01_mttv");
+                als_upd(k, M.p);
+            };
+            auto sym_right = [&]() {  // P_R(r, c) = sum_p Xp(p, r) W(p, c)
+                launch_sym01_pairs(Um[0], Um[1], sI, C, sPp, Wb.p, s);
+                check_launch("sym01_pairs");
+                const ModePlan mp = plan_view(sPp, sR, 1, C, kTcKJ, 0, ctx.sms);
+                const KrpGen bg = single_gen(Wb.p, sPp, C);
+                const KrpGen sg = make_gen(t->pdims, static_cast<int>(t->pdims.size()),
+                                           static_cast<int>(t->pdims.size()), pk_ptrs.data(), C, ctx.ones.p);
+                enqueue_planned(*t, ctx, mp, kTcKJ, bg, sg, t->d, C, 401 * 128 + 1, -1, Pbuf.p, s, nullptr);
+            };
+            steps.push_back({sym_left, 0});
+            steps.push_back({[sym_mode] { sym_mode(0); }, 0});  // by value: sym_mode is block-local
+            steps.push_back({[sym_mode] { sym_mode(1); }, 1});
+            steps.push_back({sym_right, 2});
+            for (int k = 2; k < N; ++k) steps.push_back({[&, k] { half_step(k, 2, N); }, k});
+        } else if (!tree) {
             for (int n = 0; n < N; ++n) steps.push_back({[&, n] { mode_step(n); }, n});
         } else {
             steps.push_back({pass_left, 0});
@@ -1860,7 +1956,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
                 CK(cudaMemcpyAsync(factors_out + lo_, F.p + po, static_cast<size_t>(t->dims[k] * C) * sizeof(double),
                                    cudaMemcpyDeviceToHost, s));
                 lo_ += t->dims[k] * C;
-                po += t->pdims[k] * C;
+                po += frows[k] * C;
             }
         }
         if (done > 0) {
@@ -1877,6 +1973,7 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
                  const int64_t* factor_cols, const double* lambda, int64_t nlambda, int threads, double* out4) {
     return guarded([&] {
         if (!t) fail(DMTK_GPU_EINVAL, "fit: null tensor");
+        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
         const int N = static_cast<int>(t->dims.size());
         if (nfactors != N)  // validate_model, cp_als.cpp:74-83
             fail(DMTK_GPU_EINVAL, "model has " + std::to_string(nfactors) + " factors for an order-" +

@@ -109,6 +109,72 @@ __global__ void multittv_final_kernel(const double* __restrict__ ws, int S, long
     M[e] = t;
 }
 
+// ---------------------------------- tensors symmetric in modes 0 and 1
+// X(i, j, r) = X(j, i, r) (BASELINE config 5: each (window, subject) slice is
+// a symmetric matrix). Packed layout: pair p = j (j + 1) / 2 + i for i <= j
+// (upper triangle, i fastest), then the remaining modes r; P = I (I + 1) / 2
+// pairs, padded to Pp with zero pairs.
+
+// flag = 1 if any X(i, j, r) != X(j, i, r) (exact comparison)
+__global__ void sym01_check_kernel(const double* __restrict__ X, long long I, long long pd0, long long R,
+                                   int* __restrict__ flag) {
+    const long long per = I * I;
+    for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < per * R;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = e / per;
+        const long long ij = e - r * per;
+        const long long j = ij / I, i = ij - j * I;
+        if (i < j && X[i + pd0 * (j + I * r)] != X[j + pd0 * (i + I * r)]) *flag = 1;
+    }
+}
+
+// Xp(p, r) = X(i, j, r), i <= j; one block per (r, j), threads over i
+__global__ void sym01_pack_kernel(const double* __restrict__ X, long long I, long long pd0, long long Pp,
+                                  double* __restrict__ out) {
+    const long long r = blockIdx.x;
+    const long long j = blockIdx.y;
+    const double* src = X + pd0 * (j + I * r);
+    double* dst = out + Pp * r + j * (j + 1) / 2;
+    for (long long i = threadIdx.x; i <= j; i += blockDim.x) dst[i] = src[i];
+    if (j == I - 1)  // zero the pad pairs of this r
+        for (long long q = I * (I + 1) / 2 + threadIdx.x; q < Pp; q += blockDim.x) out[Pp * r + q] = 0.0;
+}
+
+// M(a, c) = sum_b Q(pair(a, b), c) V(b, c): the MTTKRP of mode 0 (V = U_1) or
+// mode 1 (V = U_0) from the packed partial Q(p, c) = sum_r Xp(p, r) KR(r, c)
+__global__ void sym01_mttv_kernel(const double* __restrict__ Q, long long I, int C, const double* __restrict__ V,
+                                  double* __restrict__ M) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= I * C) return;
+    const long long a = e / C;
+    const int c = static_cast<int>(e - a * C);
+    double s = 0.0;
+    for (long long b = 0; b < I; ++b) {
+        const long long lo = a < b ? a : b, hi = a < b ? b : a;
+        s += Q[(hi * (hi + 1) / 2 + lo) * C + c] * V[b * C + c];
+    }
+    M[e] = s;
+}
+
+// W(p, c) = A(i, c) B(j, c) + A(j, c) B(i, c) for i < j, A(i, c) B(i, c) on the
+// diagonal: the pair weights that replace the KRP rows of modes 0 and 1
+__global__ void sym01_pairs_kernel(const double* __restrict__ A, const double* __restrict__ B, long long I, int C,
+                                   long long Pp, double* __restrict__ W) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= Pp * C) return;
+    const long long p = e / C;
+    const int c = static_cast<int>(e - p * C);
+    if (p >= I * (I + 1) / 2) {
+        W[e] = 0.0;
+        return;
+    }
+    long long j = static_cast<long long>((sqrt(8.0 * static_cast<double>(p) + 1.0) - 1.0) * 0.5);
+    while (j * (j + 1) / 2 > p) --j;
+    while ((j + 1) * (j + 2) / 2 <= p) ++j;
+    const long long i = p - j * (j + 1) / 2;
+    W[e] = i == j ? A[i * C + c] * B[i * C + c] : A[i * C + c] * B[j * C + c] + A[j * C + c] * B[i * C + c];
+}
+
 // ----------------------------------------------------------- generic MTTKRP
 // M(i,c) partial over a chunk of j: sum_j KR(j,c) * sum_l X(l,i,j) KL(l,c).
 // Slot layout ws[(jc * I + i) * C + c]; the CSR reduce finishes the sum.
@@ -717,6 +783,26 @@ void launch_mttkrp_generic(const double* X, long long L, long long I, long long 
                            const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(n_jc), static_cast<unsigned>((I * C + 127) / 128));
     mttkrp_generic_kernel<<<grid, 128, 0, s>>>(X, L, I, R, C, kl, kr, jchunk, ws);
+}
+
+void launch_sym01_check(const double* X, long long I, long long pd0, long long R, int* flag, cudaStream_t s) {
+    sym01_check_kernel<<<148 * 8, 256, 0, s>>>(X, I, pd0, R, flag);
+}
+
+void launch_sym01_pack(const double* X, long long I, long long pd0, long long R, long long Pp, double* out,
+                       cudaStream_t s) {
+    sym01_pack_kernel<<<dim3(static_cast<unsigned>(R), static_cast<unsigned>(I)), 128, 0, s>>>(X, I, pd0, Pp, out);
+}
+
+void launch_sym01_mttv(const double* Q, long long I, int C, const double* V, double* M, cudaStream_t s) {
+    const long long n = I * C;
+    sym01_mttv_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(Q, I, C, V, M);
+}
+
+void launch_sym01_pairs(const double* A, const double* B, long long I, int C, long long Pp, double* W,
+                        cudaStream_t s) {
+    const long long n = Pp * C;
+    sym01_pairs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(A, B, I, C, Pp, W);
 }
 
 long long multittv_ws_doubles(long long A, long long dt, long long B, int C) {

@@ -22,6 +22,14 @@ void launch_krp_level(const double* P, const double* U, double* out, long long r
                       cudaStream_t s);
 void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,
                            const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s);
+// Tensors symmetric in modes 0 and 1 (kernels.cu): check, pack the upper
+// triangle (pairs p = j (j + 1) / 2 + i, padded to Pp), MTTKRP of mode 0/1 from
+// the packed partial, pair weights of (A, B).
+void launch_sym01_check(const double* X, long long I, long long pd0, long long R, int* flag, cudaStream_t s);
+void launch_sym01_pack(const double* X, long long I, long long pd0, long long R, long long Pp, double* out,
+                       cudaStream_t s);
+void launch_sym01_mttv(const double* Q, long long I, int C, const double* V, double* M, cudaStream_t s);
+void launch_sym01_pairs(const double* A, const double* B, long long I, int C, long long Pp, double* W, cudaStream_t s);
 // Multi-TTV of a dimension-tree partial (see kernels.cu): M (dt x C) from P
 // over rows a + A (i + dt b); ws holds multittv_ws_doubles(...) doubles.
 long long multittv_ws_doubles(long long A, long long dt, long long B, int C);

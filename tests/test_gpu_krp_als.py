@@ -201,3 +201,43 @@ def test_krp_device_bitwise(rows, C):
     torch.cuda.synchronize()
     host = dg.krp([t.cpu().numpy() for t in ins])
     assert np.array_equal(out.cpu().numpy(), host)
+
+
+def _sym_tensor(oracle, dims, seed):
+    """U[0,1) tensor symmetrised in modes 0 and 1 (natural order, mode 0 fastest)."""
+    x = oracle.gen_tensor(dims, seed).reshape(dims[::-1])
+    x = x + np.swapaxes(x, -1, -2)  # X(i, j, ...) + X(j, i, ...)
+    return np.ascontiguousarray(x).reshape(-1)
+
+
+@pytest.mark.parametrize("dims,rank,iters", [((8, 8, 5, 3), 3, 10), ((12, 12, 7, 5), 5, 12), ((9, 9, 4, 3, 2), 4, 8),
+                                             ((7, 7, 10), 3, 15), ((40, 40, 12, 8), 20, 25), ((101, 101, 6), 4, 5)])
+def test_cp_als_symmetric_packed_matches_reference(ref, oracle, dims, rank, iters):
+    """Tensors symmetric in modes 0/1 packed to their upper triangles (SURVEY
+    8f-4): the packed dimension-tree sweep reads about half the bytes; its fits
+    agree with the reference's CP-ALS on the full tensor within 1e-9."""
+    x = _sym_tensor(oracle, dims, 41)
+    t = dg.DenseTensor(dims, x)
+    tp = t.pack_symmetric01()
+    got = dg.cp_als(tp, AlsConfig(rank=rank, max_iters=iters, tol=0.0, seed=7))
+    want = ref.cp_als(x, dims, rank, iters, tol=0.0, seed=7)
+    f_got = np.array([r.fit.fit for r in got.trace.iters])
+    assert len(f_got) == len(want["fits"])
+    assert np.max(np.abs(f_got - want["fits"])) <= 1e-9
+    assert abs(got.trace.tensor_norm - want["norm_x"]) <= 1e-12 * want["norm_x"]
+    assert abs(dg.tensor_norm(tp) - want["norm_x"]) <= 1e-12 * want["norm_x"]
+    for u in got.model.factors:
+        assert np.allclose(np.linalg.norm(u, axis=0), 1.0, rtol=1e-12, atol=0)
+
+
+def test_pack_symmetric_validation(oracle):
+    dims = (6, 6, 4)
+    x = oracle.gen_tensor(dims, 3)  # not symmetric
+    with pytest.raises(dg.InvalidArgument):
+        dg.DenseTensor(dims, x).pack_symmetric01()
+    with pytest.raises(dg.InvalidArgument):
+        dg.DenseTensor((6, 5, 4), oracle.gen_tensor((6, 5, 4), 3)).pack_symmetric01()
+    tp = dg.DenseTensor(dims, _sym_tensor(oracle, dims, 3)).pack_symmetric01()
+    f = oracle.gen_factors(dims, 2, 1)
+    with pytest.raises(dg.InvalidArgument):  # packed handles only run cp_als / tensor_norm
+        dg.mttkrp(dg.MttkrpRequest(tp, f, 0))
