@@ -197,6 +197,7 @@ struct PlanCacheEntry;  // a finished ModePlan (+ boundary split) per routing ke
 
 struct CsrPlan {
     long long rows = 0;
+    long long nslots = 0;  // total slots (picks the reduction kernel's shape)
     DevBufLL rowptr, slots;
     long long ws_doubles = 0;
 };
@@ -618,6 +619,7 @@ static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& m
                            ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     plan->ws_doubles = mp.ws_doubles;
+    plan->nslots = static_cast<long long>(slots.size());
     CsrPlan& ref = *plan;
     t.csr[key] = std::move(plan);
     return ref;
@@ -749,7 +751,7 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         check_launch("mttkrp_tc");
     }
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
-    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s);
+    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s, csr.nslots);
     check_launch("slot_reduce");
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
 }

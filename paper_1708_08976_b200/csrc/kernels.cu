@@ -141,19 +141,28 @@ __global__ void sym01_pack_kernel(const double* __restrict__ X, long long I, lon
 }
 
 // M(a, c) = sum_b Q(pair(a, b), c) V(b, c): the MTTKRP of mode 0 (V = U_1) or
-// mode 1 (V = U_0) from the packed partial Q(p, c) = sum_r Xp(p, r) KR(r, c)
-__global__ void sym01_mttv_kernel(const double* __restrict__ Q, long long I, int C, const double* __restrict__ V,
-                                  double* __restrict__ M) {
-    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= I * C) return;
-    const long long a = e / C;
-    const int c = static_cast<int>(e - a * C);
+// mode 1 (V = U_0) from the packed partial Q(p, c) = sum_r Xp(p, r) KR(r, c).
+// One block per a; thread (part, c) strides b, parts added in a fixed order.
+__global__ void __launch_bounds__(256) sym01_mttv_kernel(const double* __restrict__ Q, long long I, int C,
+                                                         const double* __restrict__ V, double* __restrict__ M) {
+    __shared__ double red[256];
+    const long long a = blockIdx.x;
+    const int parts = blockDim.x / C;
+    const int p = threadIdx.x / C;
+    const int c = threadIdx.x - p * C;
     double s = 0.0;
-    for (long long b = 0; b < I; ++b) {
-        const long long lo = a < b ? a : b, hi = a < b ? b : a;
-        s += Q[(hi * (hi + 1) / 2 + lo) * C + c] * V[b * C + c];
+    if (p < parts)
+        for (long long b = p; b < I; b += parts) {
+            const long long lo = a < b ? a : b, hi = a < b ? b : a;
+            s += Q[(hi * (hi + 1) / 2 + lo) * C + c] * V[b * C + c];
+        }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < C) {
+        double t = 0.0;
+        for (int q = 0; q < parts; ++q) t += red[q * C + threadIdx.x];
+        M[a * C + threadIdx.x] = t;
     }
-    M[e] = s;
 }
 
 // W(p, c) = A(i, c) B(j, c) + A(j, c) B(i, c) for i < j, A(i, c) B(i, c) on the
@@ -224,6 +233,20 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
         for (int q = 0; q < P; ++q) t += part[q * C + threadIdx.x];
         out[i * C + threadIdx.x] = t;
     }
+}
+
+// Thin variant for maps with a few slots per row (K-major views with many
+// output rows): one thread per (row, column), the row's slots in CSR order.
+__global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
+                                        const long long* __restrict__ slots, long long rows, int C,
+                                        double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= rows * C) return;
+    const long long i = e / C;
+    const int c = static_cast<int>(e - i * C);
+    double t = 0.0;
+    for (long long k = rowptr[i]; k < rowptr[i + 1]; ++k) t += ws[slots[k] * C + c];
+    out[e] = t;
 }
 
 // ----------------------------------------------------------- baseline reorder
@@ -406,6 +429,150 @@ __global__ void cholesky_inverse_kernel(const double* __restrict__ H, int n, dou
         Hinv[e] = t;
     }
     if (lane == 0) flag[0] = 1;
+}
+
+// Right-looking version for n <= 32 (one warp, lane i owns row i of the
+// working matrix and column i of L^-1, shared memory with an odd pitch):
+// at step j every lane applies its L[i][j] L[k][j] terms at once. Entry
+// (i, k) still receives its subtractions in ascending j, the same operations
+// in the same order as the left-looking cholesky_inverse_kernel, so the
+// results are bitwise the same; only the dependent chains are shorter.
+// Loops stay rolled: fully unrolled shuffle code overflowed the instruction
+// cache (measured 35 us against 15).
+__global__ void __launch_bounds__(32) cholesky_inverse_rl_kernel(const double* __restrict__ H, int n,
+                                                                 double* __restrict__ Hinv, int* __restrict__ flag) {
+    constexpr int LDA = 33;
+    __shared__ double A[32 * LDA];  // lower triangle becomes L
+    __shared__ double X[32 * LDA];  // X[j][c] = L^-1[j][c]
+    const int lane = threadIdx.x;
+    for (int k = 0; k < n; ++k) {
+        A[lane * LDA + k] = lane < n ? __ldg(H + lane * n + k) : 0.0;
+        X[k * LDA + lane] = k == lane ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    double tr = 0.0;
+    for (int k = 0; k < n; ++k) tr += A[k * LDA + k];
+    const double tol = 1e-12 * tr;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+        const double d = A[j * LDA + j];
+        if (d <= tol) {  // uniform
+            if (lane == 0) flag[0] = 0;
+            return;
+        }
+        const double root = sqrt(d);
+        __syncwarp();
+        if (lane == j) A[j * LDA + j] = root;
+        if (lane > j && lane < n) A[lane * LDA + j] = A[lane * LDA + j] / root;
+        __syncwarp();
+        if (lane > j && lane < n) {
+            const double lij = A[lane * LDA + j];
+#pragma unroll 4
+            for (int k = j + 1; k <= lane; ++k) A[lane * LDA + k] -= lij * A[k * LDA + j];
+        }
+        __syncwarp();
+    }
+    // column `lane` of L^-1: x_m final at step m, then x_j -= L[j][m] x_m
+    if (lane < n) {
+#pragma unroll 1
+        for (int m = lane; m < n; ++m) {
+            const double xm = X[m * LDA + lane] / A[m * LDA + m];
+            X[m * LDA + lane] = xm;
+#pragma unroll 4
+            for (int j = m + 1; j < n; ++j) X[j * LDA + lane] -= A[j * LDA + m] * xm;
+        }
+    }
+    __syncwarp();
+    // H^-1[a][b] = sum_{k >= max(a, b)} X[k][a] X[k][b], k ascending
+    if (lane < n) {
+#pragma unroll 1
+        for (int bcol = 0; bcol < n; ++bcol) {
+            double t = 0.0;
+            for (int k = lane > bcol ? lane : bcol; k < n; ++k) t += X[k * LDA + lane] * X[k * LDA + bcol];
+            Hinv[lane * n + bcol] = t;
+        }
+    }
+    if (lane == 0) flag[0] = 1;
+}
+
+// The CP-ALS solve for n <= 32 in one 256-thread CTA, laid out for B200's
+// long FP64 dependent latency (~100 cycles per DFMA, ~140 per division,
+// ~190 per square root; tools/probe/lat_probe.cu): only the Cholesky pivot
+// sequence and the per-column substitutions stay serial.
+//   phase 0  H = Hadamard of the cached Grams but `skip` (hadamard_grams_kernel
+//            order), kept in shared memory and written out for the fit
+//   phase 1  right-looking Cholesky by warp 0 (entry (i, k) gets its
+//            subtractions in ascending j: the left-looking kernel's operations)
+//   phase 2  column c of L^-1 by thread c (forward substitution, ascending)
+//   phase 3  H^-1[a][b] = sum_{k >= max(a, b)} L^-1[k][a] L^-1[k][b], one
+//            entry per thread
+__global__ void __launch_bounds__(256) als_solve_kernel(const double* __restrict__ grams, int nmodes, int skip, int n,
+                                                        double* __restrict__ Hout, double* __restrict__ Hinv,
+                                                        int* __restrict__ flag) {
+    constexpr int LDA = 33;
+    __shared__ double A[32 * LDA];
+    __shared__ double X[32 * LDA];
+    __shared__ int s_ok;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        double h = 1.0;
+        for (int k = 0; k < nmodes; ++k)
+            if (k != skip) h *= grams[static_cast<long long>(k) * n * n + e];
+        Hout[e] = h;
+        const int i = e / n, k = e - (e / n) * n;
+        A[i * LDA + k] = h;
+        X[i * LDA + k] = i == k ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const int lane = tid;
+        double tr = 0.0;
+        for (int k = 0; k < n; ++k) tr += A[k * LDA + k];
+        const double tol = 1e-12 * tr;
+        int ok = 1;
+#pragma unroll 1
+        for (int j = 0; j < n; ++j) {
+            const double d = A[j * LDA + j];
+            if (d <= tol) {
+                ok = 0;
+                break;
+            }
+            const double root = sqrt(d);
+            __syncwarp();
+            if (lane == j) A[j * LDA + j] = root;
+            if (lane > j && lane < n) A[lane * LDA + j] = A[lane * LDA + j] / root;
+            __syncwarp();
+            if (lane > j && lane < n) {
+                const double lij = A[lane * LDA + j];
+#pragma unroll 4
+                for (int k = j + 1; k <= lane; ++k) A[lane * LDA + k] -= lij * A[k * LDA + j];
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (tid == 0) flag[0] = 0;
+        return;
+    }
+    if (tid < n) {
+#pragma unroll 1
+        for (int m = tid; m < n; ++m) {
+            const double xm = X[m * LDA + tid] / A[m * LDA + m];
+            X[m * LDA + tid] = xm;
+#pragma unroll 4
+            for (int j = m + 1; j < n; ++j) X[j * LDA + tid] -= A[j * LDA + m] * xm;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int a = e / n, b = e - (e / n) * n;
+        double t = 0.0;
+        for (int k = a > b ? a : b; k < n; ++k) t += X[k * LDA + a] * X[k * LDA + b];
+        Hinv[e] = t;
+    }
+    if (tid == 0) flag[0] = 1;
 }
 
 // U = M H^-1, one output element per thread (H^-1 staged in shared memory).
@@ -795,8 +962,7 @@ void launch_sym01_pack(const double* X, long long I, long long pd0, long long R,
 }
 
 void launch_sym01_mttv(const double* Q, long long I, int C, const double* V, double* M, cudaStream_t s) {
-    const long long n = I * C;
-    sym01_mttv_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(Q, I, C, V, M);
+    sym01_mttv_kernel<<<static_cast<unsigned>(I), 256, 0, s>>>(Q, I, C, V, M);
 }
 
 void launch_sym01_pairs(const double* A, const double* B, long long I, int C, long long Pp, double* W,
@@ -825,8 +991,14 @@ void launch_multittv(const double* P, int C, long long A, long long dt, long lon
 }
 
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
-                        double* out, cudaStream_t s) {
+                        double* out, cudaStream_t s, long long nslots) {
     if (rows <= 0) return;
+    if (nslots <= 8 * rows) {  // a few slots per row: one thread per (row, column), rows in order
+        const long long n = rows * C;
+        slot_reduce_thin_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, rowptr, slots, rows, C,
+                                                                                       out);
+        return;
+    }
     slot_reduce_kernel<<<static_cast<unsigned>(rows), kReduceThreads, 0, s>>>(ws, rowptr, slots, C, out);
 }
 
@@ -900,7 +1072,10 @@ void launch_solve_psd_inverse(const double* H, int n, const double* M, long long
     static std::atomic<unsigned long long> opted{0};
     if (first_on_device(opted))
         cudaFuncSetAttribute(cholesky_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
-    cholesky_inverse_kernel<<<1, 32, sm2, s>>>(H, n, Hinv, flag);
+    if (n <= 32)
+        cholesky_inverse_rl_kernel<<<1, 32, 0, s>>>(H, n, Hinv, flag);
+    else
+        cholesky_inverse_kernel<<<1, 32, sm2, s>>>(H, n, Hinv, flag);
     const long long tot = rows * n;
     apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, n * n * 8, s>>>(Hinv, n, M, rows, U, flag);
     jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
@@ -913,6 +1088,21 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
     // (a single-CTA fusion of these steps was measured slower: one CTA's
     // latency chains cost more than the launches it saves)
     static const bool exact = std::getenv("DMTK_GPU_ALS_EXACT_SOLVE") != nullptr;
+    if (!exact && C <= 32) {  // Hadamard + Cholesky + H^-1 in one CTA, then U = M H^-1
+        double* Hinv = scratch;
+        double* V = scratch + 64 * 64;
+        double* gain = V + 64 * 64;
+        als_solve_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
+        const long long tot = rows * C;
+        apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, C * C * 8, s>>>(Hinv, C, M, rows, U,
+                                                                                            flag);
+        jacobi_kernel<<<1, 64, 0, s>>>(H, C, V, gain, flag);
+        const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
+        jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, C, M, rows, U, flag);
+        launch_normalize_cols(U, rows, C, lambda, s);
+        launch_gram(U, rows, C, Gn, s);
+        return 6;
+    }
     launch_hadamard_grams(grams, nmodes, C, skip, H, s);
     if (exact)
         launch_solve_psd(H, C, M, rows, U, scratch, flag, s);

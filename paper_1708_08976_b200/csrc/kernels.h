@@ -35,8 +35,9 @@ void launch_sym01_pairs(const double* A, const double* B, long long I, int C, lo
 long long multittv_ws_doubles(long long A, long long dt, long long B, int C);
 void launch_multittv(const double* P, int C, long long A, long long dt, long long B, const KrpGen& kl,
                      const KrpGen& kr, double* ws, double* M, cudaStream_t s);
+// nslots: total slots of the CSR map (few per row: one thread per (row, c))
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
-                        double* out, cudaStream_t s);
+                        double* out, cudaStream_t s, long long nslots);
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s);
 void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);

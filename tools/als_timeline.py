@@ -20,14 +20,19 @@ def main():
     ap.add_argument("--dims", default="100,100,1200,80")
     ap.add_argument("--rank", type=int, default=20)
     ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--tree", action="store_true")
+    ap.add_argument("--sym", action="store_true")
     a = ap.parse_args()
     dims = tuple(int(d) for d in a.dims.split(","))
     x = fmri_tensor(dims)
     t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
-    dg.cp_als(t, dg.AlsConfig(rank=a.rank, max_iters=2, tol=0.0, seed=1))
+    if a.sym:
+        t = t.pack_symmetric01()
+    cfg = lambda n: dg.AlsConfig(rank=a.rank, max_iters=n, tol=0.0, seed=1, dimension_tree=a.tree)
+    dg.cp_als(t, cfg(2))
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        dg.cp_als(t, dg.AlsConfig(rank=a.rank, max_iters=a.iters, tol=0.0, seed=1))
+        dg.cp_als(t, cfg(a.iters))
         torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ev.sort(key=lambda e: e.time_range.start)
@@ -48,7 +53,7 @@ def main():
         print(f"  {k:40s} {v:9.1f} us")
     gaps.sort(reverse=True)
     print("largest gaps (us, next kernel, at):")
-    for g in gaps[:12]:
+    for g in gaps[:20]:
         print(f"  {g[0]:8.1f} before {g[1]:40s} at {g[2]:9.1f}")
     # gap histogram
     tot = {}
