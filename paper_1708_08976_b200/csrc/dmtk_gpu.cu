@@ -516,8 +516,9 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
     }
     p.max_seg = max_seg;
     mp.ws_doubles = static_cast<long long>(mp.grid) * max_seg * tc_bm(p.RB) * C;
-    // one tile epilogue costs about one stage
-    mp.cost = tcost * static_cast<double>(p.stages_per_tile + 1) / static_cast<double>(p.stages_per_tile);
+    // a tile epilogue (accumulators out, multi-TTV scaling, slot writes) costs
+    // about three stages
+    mp.cost = tcost * static_cast<double>(p.stages_per_tile + 3) / static_cast<double>(p.stages_per_tile);
     return mp;
 }
 
@@ -863,15 +864,22 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                 pre = plan_mode(dims, mode, C, kind, ctx.sms);
                 static const bool no_swap = std::getenv("DMTK_GPU_NO_SWAP") != nullptr;
                 if (pre.kind != kGeneric && !no_swap) {
+                    // the cheapest split s, taken when it beats the 1-step view by 3%
+                    ModePlan best;
+                    int bs = 0;
                     for (int sp = 1; sp <= N - 2; ++sp) {
                         ModePlan cand = m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM,
                                                        1, ctx.sms)
                                            : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C,
                                                        kTcKJ, 1, ctx.sms);
-                        if (cand.kind != kGeneric && cand.cost < pre.cost * 0.97) {
-                            pre = cand;
-                            best_s = sp;
+                        if (cand.kind != kGeneric && (bs == 0 || cand.cost < best.cost)) {
+                            best = cand;
+                            bs = sp;
                         }
+                    }
+                    if (bs > 0 && best.cost < pre.cost * 0.97) {
+                        pre = best;
+                        best_s = bs;
                     }
                 }
                 pre.variant = best_s;
