@@ -23,6 +23,8 @@ CONFIGS = {
     "fmri20": ((100, 100, 1200, 80), 20),
     "odd25": ((999, 1001, 997), 25),
     "1000c100": ((1000, 1000, 1000), 100),
+    "km_short": ((100, 100, 100000), 25),
+    "km_mid": ((1000, 100, 10000), 25),
 }
 ALGOS = {"auto": (A.automatic, O.automatic), "one": (A.one_step, O.automatic), "left": (A.two_step, O.left),
          "right": (A.two_step, O.right), "base": (A.baseline, O.automatic)}
