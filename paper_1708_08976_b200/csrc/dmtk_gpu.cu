@@ -349,7 +349,7 @@ static double tile_cost(int RB, int G) {
 }
 
 static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int nb, int tail,
-                             int max_g_rb2, double* cost_out) {
+                             int max_g_rb2, double* cost_out, bool bj1 = false) {
     Tiling best{2, 1, 128, 1};
     double best_cost = 1e300;
     static const int force_g = [] {
@@ -358,6 +358,10 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
     }();
     static const int force_rb = [] {
         const char* e = std::getenv("DMTK_GPU_FORCE_RB");
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int force_bi = [] {
+        const char* e = std::getenv("DMTK_GPU_FORCE_BI");
         return e ? std::atoi(e) : 0;
     }();
     for (int RB : {4, 3, 2}) {
@@ -370,7 +374,7 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
             const double shape = tile_cost(RB, G);
             if (flavor == kKMajorJ) {
                 for (int bi = TR; bi >= 1; bi /= 2) {
-                    if (TR % bi) continue;
+                    if (TR % bi || (force_bi && bi != force_bi && TR % force_bi == 0) || (bj1 && bi != TR)) continue;
                     const int bj = TR / bi;
                     const double area = static_cast<double>(((rows_or_I + bi - 1) / bi) * bi) *
                                         static_cast<double>(((R + bj - 1) / bj) * bj);
@@ -396,7 +400,8 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
 }
 
 // Flavor for (mode, resolved algorithm, order) on the collapsed view.
-static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms);
+static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms,
+                          bool bj1 = false);
 
 static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, int kind_req, int sms) {
     const int N = static_cast<int>(dims.size());
@@ -405,7 +410,7 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
 
 // Plan on the collapsed view X(l, i, j); swap selects the boundary 2-step
 // epilogue (mttkrp_plan.h): output rows L (M-major) or R (K-major).
-static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms) {
+static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms, bool bj1) {
     ModePlan mp;
     mp.L = L;
     mp.I = I;
@@ -455,7 +460,7 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
         tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g, &tcost);
     } else if (mp.kind == kTcKJ) {
         p.flavor = kKMajorJ;
-        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g, &tcost);
+        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g, &tcost, bj1);
     } else {
         p.flavor = kKMajorJK;
         tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g, &tcost);
@@ -723,6 +728,16 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
             mp.tc.hrows = hr;
         }
 
+        // one-flavor epilogue instantiation (DMTK_GPU_EPI_GEN: always the general kernel)
+        static const bool epi_gen = std::getenv("DMTK_GPU_EPI_GEN") != nullptr;
+        mp.tc.epi = kEpiGen;
+        if (!epi_gen) {
+            if (mp.tc.flavor == kKMajorJ && mp.tc.swap && mp.tc.BI >= 8 * mp.tc.RB && sgen.nf == 1) {
+                mp.tc.epi = kEpiSwr;
+            } else if (mp.nb <= 3 && !mp.tc.swap) {  // instantiated up to 3 column groups
+                mp.tc.epi = mp.tc.flavor == kMMajor ? kEpiMM : (mp.tc.flavor == kKMajorJ ? kEpiKJ : kEpiJK);
+            }
+        }
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
         mp.tc.X = X;
         static const bool force_ldgsts = std::getenv("DMTK_GPU_FORCE_LDGSTS") != nullptr;
@@ -791,6 +806,89 @@ static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
     t.maps.clear();
 }
 
+// CSR slot-map cache key of a planned view: mode, boundary split, flavor and
+// (for a K-major boundary view) whether its row tile is BJ = 1.
+static int csr_key_of(int plan_mode_key, const ModePlan& mp, int kind) {
+    return (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0) +
+           (kind == kTcKJ && mp.variant > 0 && mp.tc.BJ == 1 ? 2 : 0);
+}
+
+// ----------------------------------------------- measured view selection
+// Boundary modes have several equivalent views (1-step, or the boundary
+// 2-step split at s, K-major row tiles BI x BJ). The cost model ranks them by
+// padding and builder pressure but not by DRAM behaviour, which differs by
+// up to 1.45x between views of one shape (1000^3 last mode, C = 16: 1.80 ms
+// on the 1-step view, 1.25 ms on the s = 1 view with BJ = 1). For tensors of
+// at least kTuneBytes the candidates within 1.3x of the best modelled cost
+// are timed once per (shape, mode, rank) in the process and the fastest is
+// kept (DMTK_GPU_AUTOTUNE=0 turns this off). Never while a graph is captured.
+struct TuneKey {
+    std::vector<long long> pdims;
+    int mode, C;
+    bool aligned;
+    bool operator<(const TuneKey& o) const {
+        return std::tie(pdims, mode, C, aligned) < std::tie(o.pdims, o.mode, o.C, o.aligned);
+    }
+};
+struct TuneChoice {
+    int s = 0;
+    bool bj1 = false;
+};
+static std::mutex g_tune_mu;
+static std::map<TuneKey, TuneChoice> g_tune;
+constexpr long long kTuneBytes = 256LL << 20;
+
+static bool tune_lookup(const TuneKey& k, TuneChoice& c) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tune.find(k);
+    if (it == g_tune.end()) return false;
+    c = it->second;
+    return true;
+}
+static void tune_store(const TuneKey& k, const TuneChoice& c) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tune[k] = c;
+}
+static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s) {
+    static const bool off = [] {
+        const char* e = std::getenv("DMTK_GPU_AUTOTUNE");
+        return e && std::string(e) == "0";
+    }();
+    static const long long min_bytes = [] {  // DMTK_GPU_TUNE_BYTES: threshold override (tests)
+        const char* e = std::getenv("DMTK_GPU_TUNE_BYTES");
+        return e ? std::atoll(e) : kTuneBytes;
+    }();
+    if (off || t.ptotal * 8 < min_bytes) return false;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return false;
+    return true;
+}
+
+// One warm run (slot map, tensor map, head table), then the fastest of three
+// timed runs.
+static float time_planned(dmtk_gpu_tensor_s& t, Context& ctx, const ModePlan& mp, int kind, const KrpGen& bgen,
+                          const KrpGen& sgen, const double* X, int C, int csr_key, int mode, double* dout,
+                          cudaStream_t s) {
+    constexpr int kReps = 3;
+    cudaEvent_t ev[kReps + 1];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, csr_key, mode, dout, s, nullptr);
+    CK(cudaEventRecord(ev[0], s));
+    for (int r = 0; r < kReps; ++r) {
+        enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, csr_key, mode, dout, s, nullptr);
+        CK(cudaEventRecord(ev[r + 1], s));
+    }
+    CK(cudaEventSynchronize(ev[kReps]));
+    float best = 1e30f;
+    for (int r = 0; r < kReps; ++r) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[r], ev[r + 1]));
+        best = std::min(best, ms);
+    }
+    for (auto& e : ev) CK(cudaEventDestroy(e));
+    return best;
+}
+
 static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double* const* dU, int C, int mode, int algo,
                            int order, double* dout, cudaStream_t s, Phases* ph) {
     const int N = static_cast<int>(t.dims.size());
@@ -856,6 +954,24 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
             have_pre = true;
             int best_s = 0;
             const long long pkey = ((static_cast<long long>(mode) * 8 + algo) * 8 + order) * 4096 + C;
+            // B and scale generators of the 1-step view (sp = 0) or the boundary 2-step view split at sp
+            auto gens_for = [&](int sp, KrpGen& bg, KrpGen& sg) {
+                if (sp == 0) {
+                    bg = m0 ? make_gen(dims, 1, N, dU, C, ones) : make_gen(dims, 0, mode, dU, C, ones);
+                    sg = m0 ? make_gen(dims, 0, 0, dU, C, ones) : make_gen(dims, N, N, dU, C, ones);
+                } else if (m0) {
+                    bg = make_gen(dims, sp + 1, N, dU, C, ones);
+                    sg = make_gen(dims, 1, sp + 1, dU, C, ones);
+                } else {
+                    bg = make_gen(dims, 0, sp, dU, C, ones);
+                    sg = make_gen(dims, sp, N - 1, dU, C, ones);
+                }
+            };
+            auto swap_view = [&](int sp, bool bj1) {
+                return m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM, 1, ctx.sms)
+                          : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C, kTcKJ, 1, ctx.sms,
+                                      bj1);
+            };
             auto pit = t.plans.find(pkey);
             if (pit != t.plans.end()) {
                 pre = pit->second->mp;
@@ -863,23 +979,80 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
             } else {
                 pre = plan_mode(dims, mode, C, kind, ctx.sms);
                 static const bool no_swap = std::getenv("DMTK_GPU_NO_SWAP") != nullptr;
+                static const int force_s = [] {
+                    const char* e = std::getenv("DMTK_GPU_FORCE_SWAP");
+                    return e ? std::atoi(e) : 0;
+                }();
                 if (pre.kind != kGeneric && !no_swap) {
+                    const ModePlan one_step = pre;
                     // the cheapest split s, taken when it beats the 1-step view by 3%
                     ModePlan best;
                     int bs = 0;
                     for (int sp = 1; sp <= N - 2; ++sp) {
-                        ModePlan cand = m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM,
-                                                       1, ctx.sms)
-                                           : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C,
-                                                       kTcKJ, 1, ctx.sms);
+                        ModePlan cand = swap_view(sp, false);
                         if (cand.kind != kGeneric && (bs == 0 || cand.cost < best.cost)) {
                             best = cand;
                             bs = sp;
                         }
                     }
+                    if (force_s >= 1 && force_s <= N - 2) {  // developer switch: this split, if it plans
+                        ModePlan cand = swap_view(force_s, false);
+                        if (cand.kind != kGeneric) {
+                            best = cand;
+                            bs = force_s;
+                            pre.cost = 1e300;
+                        }
+                    }
                     if (bs > 0 && best.cost < pre.cost * 0.97) {
                         pre = best;
                         best_s = bs;
+                    }
+                    // Large tensors: the modelled choice misses DRAM effects (K-major
+                    // tiles whose rows lie megabytes apart stream at ~4.5 TB/s), so
+                    // the candidates are timed once per shape and the fastest kept
+                    if (force_s == 0 && tune_enabled(t, s)) {
+                        const TuneKey tk{t.pdims, mode, C, t.d != nullptr && (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
+                        TuneChoice tc;
+                        if (!tune_lookup(tk, tc)) {
+                            std::vector<std::pair<ModePlan, TuneChoice>> cands{{one_step, {0, false}}};
+                            for (int sp = 1; sp <= N - 2; ++sp)
+                                for (bool bj1 : {false, true}) {
+                                    if (bj1 && m0) continue;
+                                    ModePlan cand = swap_view(sp, bj1);
+                                    if (cand.kind == kGeneric || (bj1 && cand.tc.BJ != 1)) continue;
+                                    if (!bj1 && !m0 && cand.tc.BJ == 1) continue;  // same as the bj1 candidate
+                                    cands.push_back({cand, {sp, bj1}});
+                                }
+                            double cmin = 1e300;
+                            for (auto& c : cands) cmin = std::min(cmin, c.first.cost);
+                            // the modelled choice is kept unless another view is 2% faster
+                            float tbest = 1e30f;
+                            for (auto& c : cands) {
+                                const bool modelled = c.second.s == best_s && c.first.tc.BI == pre.tc.BI &&
+                                                      c.first.tc.BJ == pre.tc.BJ && c.first.tc.RB == pre.tc.RB;
+                                if (c.first.cost > 1.3 * cmin && !modelled) continue;  // padding timing would not recover
+                                KrpGen bg, sg;
+                                gens_for(c.second.s, bg, sg);
+                                ModePlan cp = c.first;
+                                cp.variant = c.second.s;
+                                if (mode == 0) cp.out_rows = std::min(cp.out_rows, t.dims[0]);
+                                const float ms = time_planned(t, ctx, cp, kind, bg, sg, X, C,
+                                                              csr_key_of(mode, cp, kind), mode, dout, s) *
+                                                 (modelled ? 0.98f : 1.0f);
+                                if (ms < tbest) {
+                                    tbest = ms;
+                                    tc = c.second;
+                                }
+                            }
+                            tune_store(tk, tc);
+                        }
+                        if (tc.s == 0) {
+                            pre = one_step;
+                            best_s = 0;
+                        } else {
+                            pre = swap_view(tc.s, tc.bj1);
+                            best_s = tc.s;
+                        }
                     }
                 }
                 pre.variant = best_s;
@@ -888,16 +1061,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                 e->best_s = best_s;
                 t.plans[pkey] = std::move(e);
             }
-            if (best_s == 0) {
-                bgen = m0 ? make_gen(dims, 1, N, dU, C, ones) : make_gen(dims, 0, mode, dU, C, ones);
-                sgen = m0 ? make_gen(dims, 0, 0, dU, C, ones) : make_gen(dims, N, N, dU, C, ones);
-            } else if (m0) {
-                bgen = make_gen(dims, best_s + 1, N, dU, C, ones);
-                sgen = make_gen(dims, 1, best_s + 1, dU, C, ones);
-            } else {
-                bgen = make_gen(dims, 0, best_s, dU, C, ones);
-                sgen = make_gen(dims, best_s, N - 1, dU, C, ones);
-            }
+            gens_for(best_s, bgen, sgen);
         } else {
             kind = kTcKJK;
             bgen = make_gen(dims, 0, mode, dU, C, ones);
@@ -972,8 +1136,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
     }
     if (mode == 0) mp.out_rows = std::min(mp.out_rows, t.dims[0]);  // drop a pad row
     const int plan_mode_key = algo == DMTK_GPU_BASELINE ? 100 + mode : mode;
-    enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, (plan_mode_key * 16 + mp.variant) * 8 + (kind == kTcKJ ? 1 : 0),
-                    mode, dout, s, ph);
+    enqueue_planned(t, ctx, mp, kind, bgen, sgen, X, C, csr_key_of(plan_mode_key, mp, kind), mode, dout, s, ph);
 }
 
 // Ranks above 64 (the kernels' register budget) run as column chunks of at

@@ -78,6 +78,17 @@ struct TcPlan {
     const double* X;          // tensor base (the LDGSTS producer reads it directly)
     int ldgsts;               // 1: strides or base not 16-byte aligned for TMA; the producer warp
                               // copies the swizzled stage with 8-byte cp.async instead
+    int epi;                  // epilogue instantiation (Epi): kEpiGen compiles every flavor's epilogue,
+                              // the others only their own (fewer live registers in the consumer loop)
+};
+
+// Epilogue instantiations of the streaming kernel (template parameter EPI).
+enum Epi : int {
+    kEpiGen = 0,  // every flavor (boundary 2-step views other than kEpiSwr)
+    kEpiSwr = 1,  // K-major boundary 2-step, BI >= 8 RB, one-factor scale: one output row per warp
+    kEpiMM = 2,   // M-major, no swap (1-step mode 0, 2-step right)
+    kEpiKJ = 3,   // K-major rows (i, j), no swap (1-step last mode, 2-step left)
+    kEpiJK = 4,   // K-major interior 1-step
 };
 
 // Stage range of CTA b under the stream-K split.

@@ -84,7 +84,8 @@ struct StageCursor {
     }
 };
 
-template <int NB, int TAIL, bool KMAJ, int RB>
+// EPI: which epilogue is compiled (Epi, mttkrp_plan.h; TcPlan::epi).
+template <int NB, int TAIL, bool KMAJ, int RB, int EPI = kEpiGen>
 __global__ void __launch_bounds__(tc_threads(RB), 1)
     mttkrp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcPlan p) {
     using Cfg = TcCfg<NB, TAIL, RB>;
@@ -640,8 +641,34 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         __syncwarp();
         const int C = p.C;
         double* wsb = p.ws + ((static_cast<long long>(blockIdx.x) * p.max_seg + seg) * Cfg::BM + RW * w) * C;
+        if constexpr (EPI == kEpiSwr) {
+            // K-major boundary 2-step, one output row j per warp (BI >= RW) and
+            // one (or a materialised) scale factor: rows read from one base
+            // pointer with 32-bit offsets, four independent partial sums (a
+            // serial chain of FP64 FMAs costs ~100 cycles per link on B200)
+            // combined pairwise in a fixed order.
+            const long long tj = div_nn(tile, p.n_ti);
+            const long long ti = tile - tj * p.n_ti;
+            const long long j = tj * p.BJ + (RW * lw) / p.BI;
+            const long long ib = ti * p.BI + (RW * lw) % p.BI;
+            const int nv = p.I - ib < RW ? static_cast<int>(p.I - ib) : RW;  // valid rows
+            const int ldu = static_cast<int>(p.sgen.ldu);
+            const double* __restrict__ sbase = p.sgen.U[0] + ib * p.sgen.ldu;
+            for (int c = lane; c < C; c += 32) {
+                double part[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int r0 = 0; r0 < RW; r0 += EC) {
+                    double sc[EC];
+#pragma unroll
+                    for (int r = 0; r < EC; ++r) sc[r] = r0 + r < nv ? __ldg(sbase + (r0 + r) * ldu + c) : 0.0;
+#pragma unroll
+                    for (int r = 0; r < EC; ++r) part[r % 4] = fma(Pw[(r0 + r) * LD + c], sc[r], part[r % 4]);
+                }
+                if (j < p.R) wsb[c] = (part[0] + part[2]) + (part[1] + part[3]);
+            }
+        } else {
         for (int c = lane; c < C; c += 32) {
-            if (!KMAJ && p.swap) {
+            if (!KMAJ && EPI == kEpiGen && p.swap) {
                 // boundary 2-step, mode 0: output row l = m % L, scale KRP(i = m / L)
                 const long long mrows = p.L * p.I;
                 const long long mbase = tile * p.TR + RW * lw;
@@ -665,7 +692,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                         }
                     }
                 }
-            } else if (KMAJ && p.swap) {
+            } else if (KMAJ && EPI == kEpiGen && p.swap) {
                 // boundary 2-step, last mode: output row j, scale KRP(i)
                 const long long tj = div_nn(tile, p.n_ti);
                 const long long ti = tile - tj * p.n_ti;
@@ -755,7 +782,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     }
                     wsb[(cur - ifirst) * C + c] = sum;
                 }
-            } else if (p.flavor == kKMajorJ) {
+            } else if (EPI == kEpiKJ || (EPI == kEpiGen && p.flavor == kKMajorJ)) {
                 const long long tj = div_nn(tile, p.n_ti);
                 const long long ti = tile - tj * p.n_ti;
                 if (p.BI >= RW) {
@@ -794,6 +821,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                 for (int r = 0; r < RW && ibase + r < p.I; ++r) wsb[r * C + c] = Pw[r * LD + c];
             }
         }
+        }  // kEpiSwr
         __syncwarp();
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {

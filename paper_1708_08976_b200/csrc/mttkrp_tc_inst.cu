@@ -20,10 +20,10 @@ namespace dmtkg {
 // with DMTK_GPU_MAX_TAIL=4) on 128-row tiles.
 constexpr bool tc_has_tail(int tail) { return tail == 0 || tail == 1 || tail == 2 || (tail == 4 && TC_RB == 2); }
 
-template <int TAIL, bool KM>
+template <int TAIL, bool KM, int EPI = kEpiGen>
 static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaStream_t s) {
     if constexpr (tc_has_tail(TAIL)) {
-        auto k = mttkrp_tc_kernel<TC_NB, TAIL, KM, TC_RB>;
+        auto k = mttkrp_tc_kernel<TC_NB, TAIL, KM, TC_RB, EPI>;
         static std::atomic<unsigned long long> opted{0};  // per device; not a stream op (graph-safe)
         if (first_on_device(opted)) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         k<<<grid, tc_threads(TC_RB), p.smem, s>>>(map, p);
@@ -32,6 +32,28 @@ static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaSt
 
 bool TC_LAUNCH(const TcPlan& p, const CUtensorMap& map, int tail, bool kmajor, int grid, cudaStream_t s) {
     if (p.RB != TC_RB || !tc_has_tail(tail)) return false;
+    // one-flavor epilogue instantiations (tails 0-2), else the general kernel;
+    // the 1-step/2-step ones only up to 3 column groups (measured 1-2% slower
+    // than the general kernel at C = 32 and 50, 1-6% faster at C <= 25)
+    if (p.epi != kEpiGen && tail <= 2 && (p.epi == kEpiMM) != kmajor) {
+        switch (p.epi * 4 + tail) {
+            case kEpiSwr * 4 + 0: launch_one<0, true, kEpiSwr>(p, map, grid, s); return true;
+            case kEpiSwr * 4 + 1: launch_one<1, true, kEpiSwr>(p, map, grid, s); return true;
+            case kEpiSwr * 4 + 2: launch_one<2, true, kEpiSwr>(p, map, grid, s); return true;
+#if TC_NB <= 3
+            case kEpiMM * 4 + 0: launch_one<0, false, kEpiMM>(p, map, grid, s); return true;
+            case kEpiMM * 4 + 1: launch_one<1, false, kEpiMM>(p, map, grid, s); return true;
+            case kEpiMM * 4 + 2: launch_one<2, false, kEpiMM>(p, map, grid, s); return true;
+            case kEpiKJ * 4 + 0: launch_one<0, true, kEpiKJ>(p, map, grid, s); return true;
+            case kEpiKJ * 4 + 1: launch_one<1, true, kEpiKJ>(p, map, grid, s); return true;
+            case kEpiKJ * 4 + 2: launch_one<2, true, kEpiKJ>(p, map, grid, s); return true;
+            case kEpiJK * 4 + 0: launch_one<0, true, kEpiJK>(p, map, grid, s); return true;
+            case kEpiJK * 4 + 1: launch_one<1, true, kEpiJK>(p, map, grid, s); return true;
+            case kEpiJK * 4 + 2: launch_one<2, true, kEpiJK>(p, map, grid, s); return true;
+#endif
+            default: break;
+        }
+    }
     switch (tail * 2 + (kmajor ? 1 : 0)) {
         case 0: launch_one<0, false>(p, map, grid, s); return true;
         case 1: launch_one<0, true>(p, map, grid, s); return true;

@@ -139,3 +139,33 @@ def test_misaligned_borrowed_base():
         torch.cuda.synchronize()
         want = ref(x, dims, f, mode)
         assert np.linalg.norm(out.cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want), mode
+
+
+def test_measured_view_selection():
+    """Boundary modes of large tensors pick among the 1-step view and the
+    boundary 2-step views (split s, K-major row tiles BI x BJ) by timing them
+    once per shape (tune_enabled, dmtk_gpu.cu). The size threshold is lowered
+    to 0 here so the timed selection, and the one-output-row epilogue
+    instantiation (kEpiSwr) of its BJ = 1 candidates, run on small shapes."""
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0")
+    shapes = ["40x40x12x8:20", "100x10x30x8:25", "8x60x50:16", "64x4x4x64:32", "9x11x13:20", "30x20x10x8:16",
+              "300x40x40:25", "20x30x600:9"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+
+
+@pytest.mark.parametrize("rb", [2, 3, 4])
+def test_one_output_row_epilogue_forced(rb):
+    """The K-major boundary 2-step view with BJ = 1 row tiles (forced split
+    s = 1 and BI = the tile height) runs the kEpiSwr instantiation; compared
+    with the general-epilogue kernel (DMTK_GPU_EPI_GEN) and numpy."""
+    for extra in ({}, {"DMTK_GPU_EPI_GEN": "1"}):
+        env = dict(os.environ, DMTK_GPU_FORCE_SWAP="1", DMTK_GPU_FORCE_RB=str(rb),
+                   DMTK_GPU_FORCE_BI=str(64 * rb), **extra)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), "30x300x20:25",
+                            "17x260x9:16", "12x70x33:7", "10x20x5x30:20"], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)

@@ -1,6 +1,6 @@
 """Per-mode MTTKRP timing on the device-resident path (developer tool).
 
-python tools/perf_modes.py [--config 1000c25] [--algos auto,one,left,right] [--reps 5]
+python tools/perf_modes.py [--config 1000c25|AxBxC:rank,...] [--algos auto,one,left,right] [--reps 5]
 Prints ms, tensor GB/s, FP64 TF/s and fraction of roofline per mode.
 """
 import argparse
@@ -41,7 +41,11 @@ def main():
     args = ap.parse_args()
     peak = dg.fp64_peak_tflops()
     for cfg in args.config.split(","):
-        dims, C = CONFIGS[cfg]
+        if cfg in CONFIGS:
+            dims, C = CONFIGS[cfg]
+        else:  # "AxBxC:rank"
+            shp, rk = cfg.split(":")
+            dims, C = tuple(int(v) for v in shp.split("x")), int(rk)
         n = 1
         for d in dims:
             n *= d
@@ -52,6 +56,7 @@ def main():
              dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x))
         s = torch.cuda.current_stream()
         modes = [int(m) for m in args.modes.split(",")] if args.modes else range(len(dims))
+        modes = [m if m >= 0 else len(dims) + m for m in modes]
         for mode in modes:
             out = torch.empty((dims[mode], C), dtype=torch.float64, device="cuda")
             for an in args.algos.split(","):
