@@ -837,8 +837,39 @@ static std::mutex g_tune_mu;
 static std::map<TuneKey, TuneChoice> g_tune;
 constexpr long long kTuneBytes = 256LL << 20;
 
+// DMTK_GPU_TUNE_CACHE=<file>: decisions persist across processes (one line
+// per key: ndim dims... mode C aligned s bj1), read on first use and appended
+// on every new decision -- e.g. so a profiler run, whose serialised launches
+// would distort the timing, replays the plain run's choices.
+static const char* tune_cache_path() {
+    static const char* p = std::getenv("DMTK_GPU_TUNE_CACHE");
+    return p && *p ? p : nullptr;
+}
+static void tune_load_locked() {
+    static bool loaded = false;
+    if (loaded) return;
+    loaded = true;
+    const char* path = tune_cache_path();
+    if (!path) return;
+    FILE* f = std::fopen(path, "r");
+    if (!f) return;
+    int nd;
+    while (std::fscanf(f, "%d", &nd) == 1 && nd > 0 && nd <= 64) {
+        TuneKey k;
+        k.pdims.resize(nd);
+        bool ok = true;
+        for (auto& d : k.pdims) ok = ok && std::fscanf(f, "%lld", &d) == 1;
+        int al = 0, sv = 0, bj = 0;
+        ok = ok && std::fscanf(f, "%d %d %d %d %d", &k.mode, &k.C, &al, &sv, &bj) == 5;
+        if (!ok) break;
+        k.aligned = al != 0;
+        g_tune[k] = TuneChoice{sv, bj != 0};
+    }
+    std::fclose(f);
+}
 static bool tune_lookup(const TuneKey& k, TuneChoice& c) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
+    tune_load_locked();
     auto it = g_tune.find(k);
     if (it == g_tune.end()) return false;
     c = it->second;
@@ -847,6 +878,14 @@ static bool tune_lookup(const TuneKey& k, TuneChoice& c) {
 static void tune_store(const TuneKey& k, const TuneChoice& c) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     g_tune[k] = c;
+    if (const char* path = tune_cache_path()) {
+        if (FILE* f = std::fopen(path, "a")) {
+            std::fprintf(f, "%d", static_cast<int>(k.pdims.size()));
+            for (long long d : k.pdims) std::fprintf(f, " %lld", d);
+            std::fprintf(f, " %d %d %d %d %d\n", k.mode, k.C, k.aligned ? 1 : 0, c.s, c.bj1 ? 1 : 0);
+            std::fclose(f);
+        }
+    }
 }
 static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s) {
     static const bool off = [] {

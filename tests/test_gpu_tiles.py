@@ -169,3 +169,19 @@ def test_one_output_row_epilogue_forced(rb):
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+
+
+def test_tune_cache_file(tmp_path):
+    """DMTK_GPU_TUNE_CACHE: the first process writes its timed decisions, a
+    second one reads and replays them (no retiming); results stay in
+    tolerance either way."""
+    cache = tmp_path / "tune.txt"
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0", DMTK_GPU_TUNE_CACHE=str(cache))
+    shapes = ["300x40x40:25", "40x40x12x8:20"]
+    for _ in range(2):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert "failures: 0" in r.stdout
+    lines = cache.read_text().split("\n")
+    assert len([l for l in lines if l.strip()]) >= 4  # boundary modes of both shapes + interior orders

@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--bw", type=float, default=6455.9)
     ap.add_argument("--modes", default="")
     ap.add_argument("--upload", action="store_true", help="upload through the host API (padded odd layouts)")
+    ap.add_argument("--profile", action="store_true",
+                    help="after warm-up, run one call per mode between cudaProfilerStart/Stop (for ncu "
+                         "--profile-from-start off) and skip the timing")
     args = ap.parse_args()
     peak = dg.fp64_peak_tflops()
     for cfg in args.config.split(","):
@@ -67,6 +70,14 @@ def main():
                                                 s.cuda_stream)
                 call()
                 torch.cuda.synchronize()
+                if args.profile:
+                    call()
+                    torch.cuda.synchronize()
+                    torch.cuda.profiler.start()
+                    call()
+                    torch.cuda.synchronize()
+                    torch.cuda.profiler.stop()
+                    continue
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 for _ in range(args.reps):
