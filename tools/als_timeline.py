@@ -51,6 +51,16 @@ def main():
     print(f"span {span:.0f} us, kernels busy {sum(busy.values()):.0f} us, idle {sum(g[0] for g in gaps):.0f} us")
     for k, v in sorted(busy.items(), key=lambda kv: -kv[1])[:14]:
         print(f"  {k:40s} {v:9.1f} us")
+    # steady state: the second half of the span (graph replays only)
+    half = t0 + span / 2
+    late = [g for g in gaps if g[2] + t0 >= half]
+    late_busy = sum(e.time_range.end - e.time_range.start for e in ev if e.time_range.start >= half)
+    print(f"second half: idle {sum(g[0] for g in late):.0f} us, busy {late_busy:.0f} us, gaps {len(late)}")
+    lt = {}
+    for g, nm, _ in late:
+        lt[nm] = lt.get(nm, 0.0) + g
+    for k, v in sorted(lt.items(), key=lambda kv: -kv[1])[:12]:
+        print(f"  late idle before {k:40s} {v:9.1f} us")
     gaps.sort(reverse=True)
     print("largest gaps (us, next kernel, at):")
     for g in gaps[:20]:
