@@ -349,7 +349,7 @@ static double tile_cost(int RB, int G) {
 }
 
 static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long long K, int nb, int tail,
-                             int max_g_rb2, double* cost_out, bool bj1 = false) {
+                             int max_g_rb2, double* cost_out, bool bj1 = false, int rb_only = 0) {
     Tiling best{2, 1, 128, 1};
     double best_cost = 1e300;
     static const int force_g = [] {
@@ -365,7 +365,7 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
         return e ? std::atoi(e) : 0;
     }();
     for (int RB : {4, 3, 2}) {
-        if (!tc_has_tile(nb, tail, RB) || (force_rb && RB != force_rb)) continue;
+        if (!tc_has_tile(nb, tail, RB) || (force_rb && RB != force_rb) || (rb_only && RB != rb_only)) continue;
         for (int G : {1, 2, 4}) {
             if (RB == 2 && G > max_g_rb2) break;
             if (force_g && G != force_g) continue;
@@ -401,7 +401,7 @@ static Tiling choose_tiling(int flavor, long long rows_or_I, long long R, long l
 
 // Flavor for (mode, resolved algorithm, order) on the collapsed view.
 static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms,
-                          bool bj1 = false);
+                          bool bj1 = false, int rb_only = 0);
 
 static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, int kind_req, int sms) {
     const int N = static_cast<int>(dims.size());
@@ -410,7 +410,8 @@ static ModePlan plan_mode(const std::vector<long long>& dims, int mode, int C, i
 
 // Plan on the collapsed view X(l, i, j); swap selects the boundary 2-step
 // epilogue (mttkrp_plan.h): output rows L (M-major) or R (K-major).
-static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms, bool bj1) {
+static ModePlan plan_view(long long L, long long I, long long R, int C, int kind_req, int swap, int sms, bool bj1,
+                          int rb_only) {
     ModePlan mp;
     mp.L = L;
     mp.I = I;
@@ -457,13 +458,13 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
     if (const char* fg = std::getenv("DMTK_GPU_MAX_G")) max_g = std::min(max_g, std::max(1, std::atoi(fg)));
     if (mp.kind == kTcM) {
         p.flavor = kMMajor;
-        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g, &tcost);
+        tl = choose_tiling(kMMajor, mp.L * mp.I, 1, mp.R, mp.nb, mp.tail, max_g, &tcost, false, rb_only);
     } else if (mp.kind == kTcKJ) {
         p.flavor = kKMajorJ;
-        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g, &tcost, bj1);
+        tl = choose_tiling(kKMajorJ, mp.I, mp.R, mp.L, mp.nb, mp.tail, max_g, &tcost, bj1, rb_only);
     } else {
         p.flavor = kKMajorJK;
-        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g, &tcost);
+        tl = choose_tiling(kKMajorJK, mp.I, 1, mp.L, mp.nb, mp.tail, max_g, &tcost, false, rb_only);
     }
     p.RB = tl.RB;
     p.BK = tc_bk(p.RB);
@@ -594,7 +595,9 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
 }
 
 static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& mp, Context& ctx) {
-    const PlanKey key{mode, mp.kind * 16 + (mp.kind == kTcKJ ? 0 : 0), C};
+    // the slot map depends on the tiling as well as the view (the measured
+    // selection can run several tilings of one view)
+    const PlanKey key{mode, ((mp.kind * 8 + mp.tc.RB) * 8 + mp.tc.G) * 512 + (mp.kind == kGeneric ? 0 : mp.tc.BI), C};
     std::lock_guard<std::mutex> lk(t.mu);
     auto it = t.csr.find(key);
     if (it != t.csr.end() && it->second->ws_doubles == mp.ws_doubles) return *it->second;
@@ -830,15 +833,16 @@ struct TuneKey {
     }
 };
 struct TuneChoice {
-    int s = 0;
-    bool bj1 = false;
+    int s = 0;         // boundary split (0 = 1-step view) or two-step order
+    bool bj1 = false;  // K-major row tiles restricted to BJ = 1
+    int rb = 0;        // tile height RB forced (0 = the modelled one)
 };
 static std::mutex g_tune_mu;
 static std::map<TuneKey, TuneChoice> g_tune;
 constexpr long long kTuneBytes = 256LL << 20;
 
 // DMTK_GPU_TUNE_CACHE=<file>: decisions persist across processes (one line
-// per key: ndim dims... mode C aligned s bj1), read on first use and appended
+// per key: ndim dims... mode C aligned s bj1 rb), read on first use and appended
 // on every new decision -- e.g. so a profiler run, whose serialised launches
 // would distort the timing, replays the plain run's choices.
 static const char* tune_cache_path() {
@@ -859,11 +863,11 @@ static void tune_load_locked() {
         k.pdims.resize(nd);
         bool ok = true;
         for (auto& d : k.pdims) ok = ok && std::fscanf(f, "%lld", &d) == 1;
-        int al = 0, sv = 0, bj = 0;
-        ok = ok && std::fscanf(f, "%d %d %d %d %d", &k.mode, &k.C, &al, &sv, &bj) == 5;
+        int al = 0, sv = 0, bj = 0, rb = 0;
+        ok = ok && std::fscanf(f, "%d %d %d %d %d %d", &k.mode, &k.C, &al, &sv, &bj, &rb) == 6;
         if (!ok) break;
         k.aligned = al != 0;
-        g_tune[k] = TuneChoice{sv, bj != 0};
+        g_tune[k] = TuneChoice{sv, bj != 0, rb};
     }
     std::fclose(f);
 }
@@ -882,7 +886,7 @@ static void tune_store(const TuneKey& k, const TuneChoice& c) {
         if (FILE* f = std::fopen(path, "a")) {
             std::fprintf(f, "%d", static_cast<int>(k.pdims.size()));
             for (long long d : k.pdims) std::fprintf(f, " %lld", d);
-            std::fprintf(f, " %d %d %d %d %d\n", k.mode, k.C, k.aligned ? 1 : 0, c.s, c.bj1 ? 1 : 0);
+            std::fprintf(f, " %d %d %d %d %d %d\n", k.mode, k.C, k.aligned ? 1 : 0, c.s, c.bj1 ? 1 : 0, c.rb);
             std::fclose(f);
         }
     }
@@ -1018,10 +1022,17 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     sg = make_gen(dims, sp, N - 1, dU, C, ones);
                 }
             };
-            auto swap_view = [&](int sp, bool bj1) {
-                return m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM, 1, ctx.sms)
+            auto swap_view = [&](int sp, bool bj1, int rb = 0) {
+                return m0 ? plan_view(dims[0], prod(dims, 1, sp + 1), prod(dims, sp + 1, N), C, kTcM, 1, ctx.sms,
+                                      false, rb)
                           : plan_view(prod(dims, 0, sp), prod(dims, sp, N - 1), dims[N - 1], C, kTcKJ, 1, ctx.sms,
-                                      bj1);
+                                      bj1, rb);
+            };
+            // the view a measured choice names (split 0 = the 1-step view)
+            auto view_of = [&](const TuneChoice& c) {
+                return c.s == 0 ? plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C, kind, 0,
+                                            ctx.sms, false, c.rb)
+                                : swap_view(c.s, c.bj1, c.rb);
             };
             auto pit = t.plans.find(pkey);
             if (pit != t.plans.end()) {
@@ -1074,6 +1085,14 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                                     if (!bj1 && !m0 && cand.tc.BJ == 1) continue;  // same as the bj1 candidate
                                     cands.push_back({cand, {sp, bj1}});
                                 }
+                            // other tile heights of the modelled view (1000^3 mode 0 at C = 16
+                            // streams at 6.5 TB/s with 128-row tiles, 5.4 with 256-row ones)
+                            for (int rb : {4, 3, 2}) {
+                                if (rb == pre.tc.RB) continue;
+                                const TuneChoice v{best_s, false, rb};
+                                ModePlan cand = view_of(v);
+                                if (cand.kind != kGeneric && cand.tc.RB == rb) cands.push_back({cand, v});
+                            }
                             double cmin = 1e300;
                             for (auto& c : cands) cmin = std::min(cmin, c.first.cost);
                             std::vector<std::function<void()>> runs;
@@ -1081,7 +1100,8 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                             int modelled = 0;
                             for (auto& c : cands) {
                                 const bool is_model = c.second.s == best_s && c.first.tc.BI == pre.tc.BI &&
-                                                      c.first.tc.BJ == pre.tc.BJ && c.first.tc.RB == pre.tc.RB;
+                                                      c.first.tc.BJ == pre.tc.BJ && c.first.tc.RB == pre.tc.RB &&
+                                                      c.first.tc.G == pre.tc.G;
                                 if (c.first.cost > 1.3 * cmin && !is_model) continue;  // padding timing would not recover
                                 if (is_model) modelled = static_cast<int>(runs.size());
                                 KrpGen bg, sg;
@@ -1098,13 +1118,8 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                             tc = picks[pick_fastest(runs, modelled, s)];
                             tune_store(tk, tc);
                         }
-                        if (tc.s == 0) {
-                            pre = one_step;
-                            best_s = 0;
-                        } else {
-                            pre = swap_view(tc.s, tc.bj1);
-                            best_s = tc.s;
-                        }
+                        pre = tc.s == 0 && tc.rb == 0 ? one_step : view_of(tc);
+                        best_s = tc.s;
                     }
                 }
                 pre.variant = best_s;
@@ -1158,12 +1173,22 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     TuneChoice tc;
                     const ModePlan pl1 = plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C, kTcKJ,
                                                    0, ctx.sms, true);
+                    auto order_view = [&](const TuneChoice& c) {
+                        return plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C,
+                                         c.s == DMTK_GPU_ORDER_RIGHT ? kTcM : kTcKJ, 0, ctx.sms, c.bj1, c.rb);
+                    };
                     if (!tune_lookup(tk, tc)) {
                         const KrpGen gr_b = make_gen(dims, mode + 1, N, dU, C, ones), gr_s = make_gen(dims, 0, mode, dU, C, ones);
                         const KrpGen gl_b = gr_s, gl_s = gr_b;
                         std::vector<std::pair<ModePlan, TuneChoice>> cands{{pr, {DMTK_GPU_ORDER_RIGHT, false}},
                                                                            {pl, {DMTK_GPU_ORDER_LEFT, false}}};
                         if (pl1.kind != kGeneric && pl.tc.BJ != 1) cands.push_back({pl1, {DMTK_GPU_ORDER_LEFT, true}});
+                        for (int rb : {4, 3, 2}) {  // other tile heights of the modelled order
+                            if (rb == chosen.tc.RB) continue;
+                            const TuneChoice v{ord, false, rb};
+                            ModePlan cand = order_view(v);
+                            if (cand.kind != kGeneric && cand.tc.RB == rb) cands.push_back({cand, v});
+                        }
                         const double cmod = chosen.cost;  // views far costlier than the modelled one are not timed
                         cands.erase(std::remove_if(cands.begin(), cands.end(),
                                                    [&](const std::pair<ModePlan, TuneChoice>& c) {
@@ -1175,7 +1200,8 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                         for (auto& c : cands) {
                             const bool r = c.second.s == DMTK_GPU_ORDER_RIGHT;
                             const int kd = r ? kTcM : kTcKJ;
-                            if (c.second.s == ord && !c.second.bj1) modelled = static_cast<int>(runs.size());
+                            if (c.second.s == ord && !c.second.bj1 && c.second.rb == 0)
+                                modelled = static_cast<int>(runs.size());
                             const KrpGen bg = r ? gr_b : gl_b, sg = r ? gr_s : gl_s;
                             const ModePlan cp = c.first;
                             const int key = csr_key_of(mode, cp, kd);
@@ -1187,7 +1213,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                         tune_store(tk, tc);
                     }
                     ord = tc.s;
-                    chosen = ord == DMTK_GPU_ORDER_RIGHT ? pr : (tc.bj1 ? pl1 : pl);
+                    chosen = tc.rb ? order_view(tc) : (ord == DMTK_GPU_ORDER_RIGHT ? pr : (tc.bj1 ? pl1 : pl));
                 }
                 auto e = std::make_unique<PlanCacheEntry>();
                 e->mp = chosen;

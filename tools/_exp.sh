@@ -1,2 +1,2 @@
-timeout 900 python tools/perf_modes.py --config 1000c25,1000c50,1000c100,odd25,180c25,64c32,fmri20,200c16 --reps 10 2>&1 | grep -v "^#"
-for f in "" "--tree" "--sym"; do echo "timeline $f"; timeout 300 python tools/als_timeline.py $f 2>&1 | tail -25; done
+export DMTK_GPU_AUTOTUNE=0
+for v in "RB=4 G=1" "RB=3 G=1" "RB=2 G=1" "RB=4 G=2" "RB=2 G=2"; do set -- $v; for d in 9 0; do echo "$v debug $d"; env DMTK_GPU_FORCE_$1 DMTK_GPU_FORCE_$2 DMTK_GPU_DEBUG=$d timeout 600 python tools/perf_modes.py --config 1000x1000x1000:16,1000x1000x1000:25 --modes 0,1 --reps 10 2>&1 | grep -v "^#" | cut -c1-100; done; done
