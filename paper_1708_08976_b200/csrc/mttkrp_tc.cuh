@@ -735,7 +735,14 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     const int rw = static_cast<int>(p.L) - l0;  // first row of the next i
                     const double* sbase = p.sgen.U[0] + c;
                     const long long ldu = p.sgen.ldu;
-                    double s0 = 0.0, s1 = 0.0;
+                    // the one-flavor instantiation splits each sum into four
+                    // independent chains (rows of the other output row add
+                    // exact zeros); the general kernel keeps one chain (its
+                    // register allocation is shared with every flavor)
+                    constexpr int K4 = EPI == kEpiMM ? 4 : 1;
+                    double s0[K4], s1[K4];
+#pragma unroll
+                    for (int q = 0; q < K4; ++q) s0[q] = s1[q] = 0.0;
 #pragma unroll
                     for (int r0 = 0; r0 < RW; r0 += EC) {
                         double sc[EC];
@@ -748,11 +755,22 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                         for (int r = 0; r < EC; ++r) {
                             const double v = Pw[(r0 + r) * LD + c] * sc[r];
-                            if (r0 + r < rw) s0 += v; else s1 += v;
+                            if (K4 == 1) {
+                                if (r0 + r < rw) s0[0] += v; else s1[0] += v;
+                            } else {
+                                const bool first = r0 + r < rw;
+                                s0[r % K4] += first ? v : 0.0;
+                                s1[r % K4] += first ? 0.0 : v;
+                            }
                         }
                     }
-                    wsb[c] = s0;
-                    if (rw < RW) wsb[C + c] = s1;
+                    double t0 = s0[0], t1 = s1[0];
+                    if (K4 == 4) {
+                        t0 = (s0[0] + s0[2]) + (s0[1] + s0[3]);
+                        t1 = (s1[0] + s1[2]) + (s1[1] + s1[3]);
+                    }
+                    wsb[c] = t0;
+                    if (rw < RW) wsb[C + c] = t1;
                 } else if (mbase < mrows) {
                     // general case: partial rows, short L, multi-factor scales
                     const long long ifirst = div_nn(mbase, p.L);
