@@ -187,7 +187,7 @@ def run_reference(args, cfg_name, dims, C):
                          "sample": f"{len(times)} single-mode passes of {cfg_name}", "cpu": model},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------ our B200 arm
@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-als", action="store_true", help="skip the BASELINE config-5 CP-ALS timing block")
+    ap.add_argument("--als-sharded", action="store_true",
+                    help="run the CP-ALS block as the sharded device-resident ALS even at one GPU (it always is at N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     dims, C = CONFIGS[args.config]
@@ -379,7 +381,7 @@ def main():
 
     # -------------------------------- BASELINE config 5: CP-ALS (info block)
     als = None
-    if world == 1 and not args.no_als:
+    if world == 1 and not args.no_als and not args.als_sharded:
         del x, t
         torch.cuda.empty_cache()
         sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -429,6 +431,51 @@ def main():
                                     "note": "modes 0/1 symmetric slices packed to upper triangles (SURVEY 8f-4): "
                                             "the dimension tree over the pair index, ~half the bytes per pass"},
                "data": "synthetic symmetric slices, unit diagonal, tanh(N(0, 0.3^2)) off-diagonal (torch, seeded)"}
+        del xf, tf
+
+    # CP-ALS over last-mode shards: weak scaling, every rank holds a
+    # 100x100x1200x80 slab of a 100x100x1200x(80 N) tensor; the loop is on the
+    # device, NCCL all-reduces inside the per-mode CUDA graphs
+    if (world > 1 or args.als_sharded) and not args.no_als and als is None:
+        try:
+            del x, t
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from perf_als import fmri_tensor
+        from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
+        fd = (100, 100, 1200, 80)
+        xf = fmri_tensor(fd, seed=1 + rank_id)
+        tf = dg.DenseTensor.from_device(fd, xf.data_ptr(), device=local, owner=xf)
+        if world == 1:  # --als-sharded on one GPU: a world-1 group for the id broadcast
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        comm = DeviceComm(local)
+        glast, lo = fd[-1] * world, fd[-1] * rank_id
+        dist_cp_als_device(tf, comm, glast, lo, dg.AlsConfig(rank=20, max_iters=2, tol=0.0, seed=1))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        rsh = dist_cp_als_device(tf, comm, glast, lo, dg.AlsConfig(rank=20, max_iters=25, tol=0.0, seed=1))
+        wall = time.perf_counter() - t0
+        its = sorted(1e3 * v for v in rsh.iter_seconds)
+        mx = torch.tensor([its[len(its) // 2], wall], dtype=torch.float64)
+        if world > 1:
+            mx = mx.to(dev)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)  # the slowest rank sets the job's time
+        nf = int(np.prod(fd)) * world
+        als = {"workload": f"fMRI-shaped 100x100x1200x{fd[-1] * world}, rank 20, 25 iterations, tol 0, "
+                           f"sharded over the subject mode on {world} GPU(s) (BASELINE config 5)",
+               "iter_ms_median": round(float(mx[0]), 3), "wall_s": round(float(mx[1]), 4),
+               "final_fit": rsh.fits[-1], "scaling": "weak", "ranks": world,
+               "roofline_iter_ms": round(4 * 8.0 * nf / world / (hbm_peak * 1e9) * 1e3, 3),
+               "path": "dmtk_gpu_cp_als_sharded: per-mode sweep on the device, NCCL all-reduces of the "
+                       "I_n x C partials, the last factor's column norms and Gram and the fit inside the "
+                       "per-mode CUDA graphs",
+               "data": "synthetic symmetric slices per rank (torch, seeded by rank)"}
+        comm.close()
         del xf, tf
 
     # ----------------- BASELINE config 0: the 3-matrix Khatri-Rao product
@@ -481,10 +528,31 @@ def main():
             "krp": krp,
             "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
 
+def _json_stdout():
+    """The JSON line is the only thing bench.py writes to stdout: anything
+    else printed to file descriptor 1 while it runs (NCCL's version banner
+    and INFO lines, library diagnostics) is sent to stderr instead, and the
+    line goes to a duplicate of the original stdout."""
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+_OUT = None
+
+
+def emit(line):
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 if __name__ == "__main__":
+    _json_stdout()
     main()

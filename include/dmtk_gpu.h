@@ -166,6 +166,32 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
                     double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
                     int* zero_tensor, double* tensor_norm_out);
 
+/* Multi-GPU CP-ALS over last-mode shards (the reference's
+ * cp_als, cp_als.cpp:122-200, with the tensor split along its slowest mode).
+ * One process per GPU; rank r's tensor handle holds the contiguous slab of
+ * last-mode rows [last_lo, last_lo + I_{N-1}^r) of a tensor whose last extent
+ * is last_extent. The library loads NCCL at run time (libnccl.so.2) and
+ * all-reduces, on its stream (inside the per-mode CUDA graphs): the I_n x C
+ * MTTKRP partials of modes n < N-1, the column sums of squares and the Gram of
+ * the row-sharded last factor, the fit's inner product and ||X||^2. Every
+ * other step runs redundantly and identically on every rank. Initialisation
+ * follows KruskalModel::random (cp_als.cpp:87-99) over the global shape, each
+ * rank keeping its rows of the last factor. factors_out: modes 0..N-2 in full,
+ * then this rank's rows of mode N-1. The per-mode sweep only (dimtree = 0, an
+ * unpacked tensor).
+ *
+ * dmtk_gpu_comm_unique_id: 128-byte NCCL id, made on one rank and broadcast
+ * by the caller (e.g. torch.distributed) to all ranks, which then call
+ * dmtk_gpu_comm_init with their rank and device. */
+typedef struct dmtk_gpu_comm_s* dmtk_gpu_comm;
+int dmtk_gpu_comm_unique_id(unsigned char* id128);
+int dmtk_gpu_comm_init(const unsigned char* id128, int rank, int world, int device, dmtk_gpu_comm* out);
+int dmtk_gpu_comm_free(dmtk_gpu_comm comm);
+int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t last_extent, int64_t last_lo,
+                            const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out, double* fits_out,
+                            double* iter_seconds_out, double* mode_seconds_out, int* n_iters, int* zero_tensor,
+                            double* tensor_norm_out);
+
 /* dmtk::fit (cp_als.hpp:79) of the model (factors, lambda) against t:
  * out4 = {fit, rel_residual, abs_residual, defined}. Validation follows
  * validate_model (cp_als.cpp:74-83) then the MTTKRP checks. */

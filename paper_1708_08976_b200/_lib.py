@@ -66,6 +66,11 @@ _SIGS = {
     "dmtk_gpu_cp_als": (C.c_int, [T, C.POINTER(AlsConfig), dp, dp, dp, dp, dp, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), dp]),
     "dmtk_gpu_fit": (C.c_int, [T, C.c_int, dpp, i64p, i64p, dp, C.c_int64, C.c_int, dp]),
+    "dmtk_gpu_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+    "dmtk_gpu_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dmtk_gpu_comm_free": (C.c_int, [C.c_void_p]),
+    "dmtk_gpu_cp_als_sharded": (C.c_int, [T, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(AlsConfig), dp, dp, dp, dp,
+                                          dp, C.POINTER(C.c_int), C.POINTER(C.c_int), dp]),
     "dmtk_gpu_fp64_peak": (C.c_int, [C.c_int, dp]),
     "dmtk_gpu_fp64_peak_sustained": (C.c_int, [C.c_int, C.c_double, dp]),
     "dmtk_gpu_launch_count": (C.c_int64, []),

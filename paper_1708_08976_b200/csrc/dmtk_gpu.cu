@@ -26,6 +26,9 @@
 #include <tuple>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/dmtk_gpu.h"
 #include "kernels.h"
 
@@ -1961,10 +1964,59 @@ int dmtk_gpu_solve_psd(int device, int64_t rank, const double* h, int64_t rows, 
     });
 }
 
-int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out,
-                    double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
-                    int* zero_tensor, double* tensor_norm_out) {
-    return guarded([&] {
+// ------------------------------------------------ last-mode shards (NCCL)
+// Multi-GPU CP-ALS: rank r holds the slab of last-mode rows
+// [lo, lo + I_{N-1}^r). NCCL is loaded at run time (the process's libnccl.so.2,
+// e.g. torch's), so the library has no link-time NCCL dependency.
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (a.h) break;
+        }
+        if (!a.h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.h, "ncclGetErrorString"));
+        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.comm_destroy || !a.error_string) a.h = nullptr;
+        return a;
+    }();
+    if (!api.h) fail(DMTK_GPU_ERUNTIME, "NCCL (libnccl.so.2) is not available");
+    return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(DMTK_GPU_ERUNTIME, std::string(what) + ": " + nccl().error_string(r));
+}
+
+struct Shard {
+    ncclComm_t comm;
+    long long last_extent;  // global extent of the last mode
+    long long last_lo;      // this rank's first last-mode row
+};
+
+static void shard_allreduce(const Shard* sh, double* p, long long n, cudaStream_t s) {
+    if (!sh || n <= 0) return;
+    nccl_check(nccl().all_reduce(p, p, static_cast<size_t>(n), ncclFloat64, ncclSum, sh->comm, s), "ncclAllReduce");
+}
+
+static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const Shard* sh, double* factors_out,
+                       double* lambda_out, double* fits_out, double* iter_seconds_out, double* mode_seconds_out,
+                       int* n_iters, int* zero_tensor, double* tensor_norm_out) {
+    {
         if (!t) fail(DMTK_GPU_EINVAL, "cp_als: null tensor");
         if (cfg->rank < 1) fail(DMTK_GPU_EINVAL, "cp_als: rank must be >= 1");
         if (cfg->max_iters < 0) fail(DMTK_GPU_EINVAL, "cp_als: max_iters must be >= 0");
@@ -1975,6 +2027,10 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             fail(DMTK_GPU_EINVAL,
                  "mttkrp_two_step: mode 0 is a boundary mode with a degenerate partial KRP; use one_step instead");
         const int C = static_cast<int>(cfg->rank);
+        if (sh && (cfg->dimtree || t->sym01))
+            fail(DMTK_GPU_EINVAL, "cp_als_sharded: only the per-mode sweep on an unpacked slab is sharded");
+        if (sh && (sh->last_lo < 0 || sh->last_lo + t->dims[N - 1] > sh->last_extent))
+            fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab's last-mode rows lie outside the global extent");
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
@@ -1996,12 +2052,34 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         {
             long long po = 0;
             for (int k = 0; k < N; ++k) {  // reference stream order; pad rows stay zero
-                for (long long e = 0; e < t->dims[k] * C; ++e) hf[po + e] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+                // sharded: the stream covers the global last factor, this rank keeps its rows
+                const bool sk = sh && k == N - 1;
+                const long long grows = sk ? sh->last_extent : t->dims[k];
+                const long long first = sk ? sh->last_lo * C : 0;
+                for (long long e = 0; e < grows * C; ++e) {
+                    const double v = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+                    const long long le = e - first;
+                    if (le >= 0 && le < t->dims[k] * C) hf[po + le] = v;
+                }
                 po += frows[k] * C;
             }
         }
 
-        const double normx = t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx);
+        // (sharded: scalars and small exchange buffers)
+        DevBuf shb;
+        shb.ensure(static_cast<size_t>(2 * 64 + 8));
+        double* sh_sumsq = shb.p;       // C column sums of squares
+        double* sh_inner = shb.p + 64;  // the fit's inner product
+        double normx = t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx);
+        if (sh) {  // ||X||^2 summed over the shards
+            const double sq = normx * normx;
+            CK(cudaMemcpyAsync(sh_inner, &sq, sizeof(double), cudaMemcpyHostToDevice, s));
+            shard_allreduce(sh, sh_inner, 1, s);
+            double tot = 0.0;
+            CK(cudaMemcpyAsync(&tot, sh_inner, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            normx = std::sqrt(tot);
+        }
         *tensor_norm_out = normx;
         *n_iters = 0;
         *zero_tensor = 0;
@@ -2038,6 +2116,7 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
             check_launch("gram");
         }
+        shard_allreduce(sh, grams + static_cast<long long>(N - 1) * C * C, static_cast<long long>(C) * C, s);
         // ALS factor update from a mode's MTTKRP Mn (cp_als.cpp:134-153):
         // Gram-Hadamard from the cached Grams, solve, normalise, refresh this
         // mode's Gram. The fit reads the last mode's M (cp_als.cpp:149-155).
@@ -2049,9 +2128,30 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             check_launch("als_update");
             if (n == N - 1) fitM = Mn;
         };
+        // Sharded last mode: its rows are this rank's; the column norms and its
+        // Gram are sums over the shards (C and C x C all-reduces).
+        auto als_upd_sharded_last = [&](int n, const double* Mn) {
+            double* Gn = grams + static_cast<long long>(n) * C * C;
+            const int nl = launch_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam, Gn, solve_scr, ctx.flag, s,
+                                             /*solve_only*/ true);
+            count_launch(nl - 1);
+            check_launch("als_update");
+            launch_col_sumsq(Um[n], t->dims[n], C, sh_sumsq, s);
+            shard_allreduce(sh, sh_sumsq, C, s);
+            launch_normalize_cols_by(Um[n], t->dims[n], C, sh_sumsq, lam, s);
+            launch_gram(Um[n], t->dims[n], C, Gn, s);
+            count_launch(3);
+            check_launch("als_update_sharded");
+            shard_allreduce(sh, Gn, static_cast<long long>(C) * C, s);
+            fitM = Mn;
+        };
         auto mode_step = [&](int n) {
             mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
-            als_upd(n, M.p);
+            if (sh && n < N - 1) shard_allreduce(sh, M.p, t->dims[n] * C, s);  // the I_n x C partials
+            if (sh && n == N - 1)
+                als_upd_sharded_last(n, M.p);
+            else
+                als_upd(n, M.p);
         };
         // Dimension tree (dmtk_gpu.h, dimtree): halves [0, h) and [h, N)
         const bool tree = cfg->dimtree != 0 && N >= 3;
@@ -2154,8 +2254,16 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
             for (int k = hsplit; k < N; ++k) steps.push_back({[&, k] { half_step(k, hsplit, N); }, k});
         }
         auto fit_step = [&]() {
-            launch_fit_cached(Um[N - 1], fitM, t->dims[N - 1], C, lam, H, grams + static_cast<long long>(N - 1) * C * C,
-                              dnorm, fitb, s);
+            if (sh) {  // <X, Y> summed over the shards
+                launch_fit_inner(Um[N - 1], fitM, t->dims[N - 1], C, lam, sh_inner, s);
+                shard_allreduce(sh, sh_inner, 1, s);
+                launch_fit_from_inner(lam, C, H, grams + static_cast<long long>(N - 1) * C * C, dnorm, sh_inner, fitb,
+                                      s);
+                count_launch(1);
+            } else {
+                launch_fit_cached(Um[N - 1], fitM, t->dims[N - 1], C, lam, H,
+                                  grams + static_cast<long long>(N - 1) * C * C, dnorm, fitb, s);
+            }
             check_launch("fit");
         };
         steps.push_back({fit_step, -1});
@@ -2256,6 +2364,68 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
         }
         CK(cudaStreamSynchronize(s));
         *n_iters = done;
+    }
+}
+
+int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out,
+                    double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
+                    int* zero_tensor, double* tensor_norm_out) {
+    return guarded([&] {
+        cp_als_run(t, cfg, nullptr, factors_out, lambda_out, fits_out, iter_seconds_out, mode_seconds_out, n_iters,
+                   zero_tensor, tensor_norm_out);
+    });
+}
+
+struct dmtk_gpu_comm_s {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, device = 0;
+};
+
+int dmtk_gpu_comm_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        if (!id128) fail(DMTK_GPU_EINVAL, "comm_unique_id: null argument");
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(id128, &id, sizeof(id));
+    });
+}
+
+int dmtk_gpu_comm_init(const unsigned char* id128, int rank, int world, int device, dmtk_gpu_comm* out) {
+    return guarded([&] {
+        if (!id128 || !out) fail(DMTK_GPU_EINVAL, "comm_init: null argument");
+        if (world < 1 || rank < 0 || rank >= world) fail(DMTK_GPU_EINVAL, "comm_init: rank out of range");
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        CK(cudaSetDevice(device));
+        auto c = std::make_unique<dmtk_gpu_comm_s>();
+        nccl_check(nccl().comm_init_rank(&c->comm, world, id, rank), "ncclCommInitRank");
+        c->rank = rank;
+        c->world = world;
+        c->device = device;
+        *out = c.release();
+    });
+}
+
+int dmtk_gpu_comm_free(dmtk_gpu_comm c) {
+    return guarded([&] {
+        if (!c) return;
+        if (c->comm) nccl().comm_destroy(c->comm);
+        delete c;
+    });
+}
+
+int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t last_extent, int64_t last_lo,
+                            const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out, double* fits_out,
+                            double* iter_seconds_out, double* mode_seconds_out, int* n_iters, int* zero_tensor,
+                            double* tensor_norm_out) {
+    return guarded([&] {
+        if (!comm) fail(DMTK_GPU_EINVAL, "cp_als_sharded: null communicator");
+        if (slab && slab->device != comm->device)
+            fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab and the communicator are on different devices");
+        const Shard sh{comm->comm, last_extent, last_lo};
+        cp_als_run(slab, cfg, &sh, factors_out, lambda_out, fits_out, iter_seconds_out, mode_seconds_out, n_iters,
+                   zero_tensor, tensor_norm_out);
     });
 }
 

@@ -826,14 +826,17 @@ __global__ void hadamard_grams_kernel(const double* __restrict__ grams, int nmod
 
 // Column 2-norms into lambda and column scaling (cp_als.cpp:101-118); one
 // CTA per column, fixed-order tree reduction.
+// sumsq_out: write the column's sum of squares and stop (a shard's partial);
+// sumsq_in: normalise by the given sums (the partials summed over the shards).
 __global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda,
-                                      const int* __restrict__ only_if_failed) {
+                                      const int* __restrict__ only_if_failed, double* __restrict__ sumsq_out = nullptr,
+                                      const double* __restrict__ sumsq_in = nullptr) {
     if (only_if_failed && only_if_failed[0]) return;
     __shared__ double red[256];
     __shared__ double s_norm;
     const int c = blockIdx.x;
     double sq = 0.0;
-    for (long long r = threadIdx.x; r < rows; r += blockDim.x) {
+    for (long long r = threadIdx.x; r < (sumsq_in ? 0 : rows); r += blockDim.x) {
         const double v = U[r * C + c];
         sq = fma(v, v, sq);
     }
@@ -843,8 +846,12 @@ __global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, in
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
+    if (sumsq_out) {
+        if (threadIdx.x == 0) sumsq_out[c] = red[0];
+        return;
+    }
     if (threadIdx.x == 0) {
-        s_norm = sqrt(red[0]);
+        s_norm = sqrt(sumsq_in ? sumsq_in[c] : red[0]);
         lambda[c] = s_norm;
     }
     __syncthreads();
@@ -860,7 +867,10 @@ __global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, in
 __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __restrict__ Mlast, long long rows, int C,
                                   const double* __restrict__ lambda, const double* __restrict__ Hlast,
                                   const double* __restrict__ Glast, const double* __restrict__ normx,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, const double* __restrict__ inner_in,
+                                  double* __restrict__ inner_out) {
+    // inner_out: write <X, Y> of these rows and stop (a shard's partial);
+    // inner_in: take <X, Y> from there (the partials summed over the shards)
     // <X, Y> from the last mode's MTTKRP and ||Y||^2 from the Grams, both as
     // fixed-order block reductions (deterministic)
     __shared__ double red[256];
@@ -870,7 +880,7 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
     __syncthreads();
     double inner = 0.0;
     const long long n = rows * C;
-    for (long long r = threadIdx.x / C, c = threadIdx.x % C; r < rows;) {
+    for (long long r = threadIdx.x / C, c = threadIdx.x % C; r < (inner_in ? 0 : rows);) {
         const long long e = r * C + c;
         inner += Mlast[e] * slam[c] * U[e];
         c += blockDim.x % C;
@@ -882,7 +892,7 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
     }
     (void)n;
     double ny = 0.0;
-    for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+    for (int e = threadIdx.x; e < (inner_out ? 0 : C * C); e += blockDim.x) {
         const int c1 = e / C, c2 = e - (e / C) * C;
         ny += slam[c1] * slam[c2] * Hlast[e] * Glast[e];
     }
@@ -896,8 +906,12 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
         }
         __syncthreads();
     }
+    if (inner_out) {
+        if (threadIdx.x == 0) inner_out[0] = red[0];
+        return;
+    }
     if (threadIdx.x == 0) {
-        const double in = red[0];
+        const double in = inner_in ? inner_in[0] : red[0];
         const double nyv = red2[0];
         const double nx = normx[0];
         double res2 = nx * nx - 2.0 * in + nyv;
@@ -1059,6 +1073,14 @@ void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, dou
     hadamard_grams_kernel<<<(C * C + 127) / 128, 128, 0, s>>>(grams, nmodes, C, skip, H);
 }
 
+void launch_col_sumsq(const double* U, long long rows, int C, double* sumsq, cudaStream_t s) {
+    normalize_cols_kernel<<<C, 256, 0, s>>>(const_cast<double*>(U), rows, C, nullptr, nullptr, sumsq, nullptr);
+}
+
+void launch_normalize_cols_by(double* U, long long rows, int C, const double* sumsq, double* lambda, cudaStream_t s) {
+    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr, nullptr, sumsq);
+}
+
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
     normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr);
 }
@@ -1084,7 +1106,8 @@ void launch_solve_psd_inverse(const double* H, int n, const double* M, long long
 }
 
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
-                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s) {
+                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s,
+                      bool solve_only) {
     // (a single-CTA fusion of these steps was measured slower: one CTA's
     // latency chains cost more than the launches it saves)
     static const bool exact = std::getenv("DMTK_GPU_ALS_EXACT_SOLVE") != nullptr;
@@ -1099,6 +1122,7 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         jacobi_kernel<<<1, 64, 0, s>>>(H, C, V, gain, flag);
         const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
         jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, C, M, rows, U, flag);
+        if (solve_only) return 4;
         launch_normalize_cols(U, rows, C, lambda, s);
         launch_gram(U, rows, C, Gn, s);
         return 6;
@@ -1108,6 +1132,7 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         launch_solve_psd(H, C, M, rows, U, scratch, flag, s);
     else
         launch_solve_psd_inverse(H, C, M, rows, U, scratch, flag, s);
+    if (solve_only) return 5;
     launch_normalize_cols(U, rows, C, lambda, s);
     launch_gram(U, rows, C, Gn, s);
     return 7;
@@ -1115,7 +1140,18 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
 
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s) {
-    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, Glast, normx, out);
+    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, Glast, normx, out, nullptr, nullptr);
+}
+
+void launch_fit_inner(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
+                      double* inner_out, cudaStream_t s) {
+    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                        inner_out);
+}
+
+void launch_fit_from_inner(const double* lambda, int C, const double* Hlast, const double* Glast,
+                           const double* normx, const double* inner, double* out, cudaStream_t s) {
+    fit_cached_kernel<<<1, 256, 0, s>>>(nullptr, nullptr, 0, C, lambda, Hlast, Glast, normx, out, inner, nullptr);
 }
 
 void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s) {

@@ -57,10 +57,20 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s);
+// sharded rows (CP-ALS over last-mode shards): a shard's column sums of squares, then the
+// normalisation by the sums over all shards
+void launch_col_sumsq(const double* U, long long rows, int C, double* sumsq, cudaStream_t s);
+void launch_normalize_cols_by(double* U, long long rows, int C, const double* sumsq, double* lambda, cudaStream_t s);
+// sharded fit: a shard's <X, Y> partial, then the fit from the summed inner product
+void launch_fit_inner(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
+                      double* inner_out, cudaStream_t s);
+void launch_fit_from_inner(const double* lambda, int C, const double* Hlast, const double* Glast,
+                           const double* normx, const double* inner, double* out, cudaStream_t s);
 // One ALS factor update (Hadamard of cached Grams, solve through H^-1,
 // normalise, new Gram). Returns the launch count.
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
-                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s);
+                      double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s,
+                      bool solve_only = false);
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s);
 

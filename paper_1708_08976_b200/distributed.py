@@ -190,3 +190,87 @@ def dist_cp_als(backend: Backend, slab: np.ndarray, dims: Sequence[int], rank: i
         prev = fit
     full = list(factors[:-1]) + [_allgather_rows(factors[-1], dims[-1], world, device)]
     return DistAlsResult(full, lam, fits, norm_x, False)
+
+
+# ------------------------------------------------ device-resident sharded CP-ALS
+@dataclass
+class ShardedAlsResult:
+    factors: List[np.ndarray]  # modes 0..N-2 in full, then this rank's rows of mode N-1
+    lambda_: np.ndarray
+    fits: List[float]
+    iter_seconds: List[float]
+    tensor_norm: float
+    zero_tensor: bool
+
+
+class DeviceComm:
+    """An NCCL communicator owned by the library (dmtk_gpu_comm_*): rank 0
+    makes the 128-byte id, torch.distributed broadcasts it, every rank joins
+    on its device. The library then all-reduces on its own stream, inside the
+    CP-ALS per-mode CUDA graphs."""
+
+    def __init__(self, device: int = 0):
+        from . import _lib
+        import ctypes as C
+        self._lib = _lib.lib
+        self._C = C
+        world, rank = dist.get_world_size(), dist.get_rank()
+        buf = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(self._lib, self._lib.dmtk_gpu_comm_unique_id(buf))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0)
+        buf = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        self.handle = C.c_void_p()
+        _check(self._lib, self._lib.dmtk_gpu_comm_init(buf, rank, world, device, C.byref(self.handle)))
+        self.rank, self.world, self.device = rank, world, device
+
+    def close(self):
+        if self.handle:
+            self._lib.dmtk_gpu_comm_free(self.handle)
+            self.handle = self._C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+def _check(lib, rc):
+    if rc != 0:
+        raise RuntimeError(lib.dmtk_gpu_last_error().decode())
+
+
+def dist_cp_als_device(slab_tensor, comm: DeviceComm, global_last: int, last_lo: int, config) -> ShardedAlsResult:
+    """The reference's cp_als (cp_als.cpp:122-200) over last-mode shards with
+    the whole loop on the device (dmtk_gpu_cp_als_sharded): slab_tensor is this
+    rank's DenseTensor (last-mode rows [last_lo, last_lo + its extent) of a
+    tensor whose last extent is global_last); config an api.AlsConfig (the
+    per-mode sweep)."""
+    from . import _lib
+    import ctypes as C
+    lib = _lib.lib
+    dims = slab_tensor.dims
+    n = len(dims)
+    rank = int(config.rank)
+    cfg = _lib.AlsConfig(rank, config.max_iters, config.tol, config.seed, config.threads, int(config.algo),
+                         int(config.order), int(bool(getattr(config, "dimension_tree", False))))
+    f = np.zeros(int(sum(dims)) * max(rank, 1))
+    lam = np.zeros(max(rank, 1))
+    cap = max(int(config.max_iters), 1)
+    fits = np.zeros(cap)
+    secs = np.zeros(cap)
+    k = C.c_int(0)
+    zero = C.c_int(0)
+    norm = np.zeros(1)
+    dp = lambda a: a.ctypes.data_as(_lib.dp)  # noqa: E731
+    _check(lib, lib.dmtk_gpu_cp_als_sharded(slab_tensor.handle(), comm.handle, int(global_last), int(last_lo),
+                                            C.byref(cfg), dp(f), dp(lam), dp(fits), dp(secs), None, C.byref(k),
+                                            C.byref(zero), dp(norm)))
+    factors, off = [], 0
+    for d in dims:
+        factors.append(f[off:off + d * rank].reshape(d, rank).copy())
+        off += d * rank
+    return ShardedAlsResult(factors, lam[:rank].copy(), list(fits[:k.value]), list(secs[:k.value]), float(norm[0]),
+                            bool(zero.value))

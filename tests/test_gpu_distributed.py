@@ -47,3 +47,43 @@ def test_gpu_backend_sharded_mttkrp_and_als(group, oracle, dims, C):
     res = dist_cp_als(be, slab, dims, 3, 6, 0.0, 11, dev)
     _, _, want_fits, _ = oracle.cp_als(x, dims, 3, 6, 0.0, 11)
     assert np.max(np.abs(np.array(res.fits) - want_fits)) <= 1e-9
+
+
+@pytest.mark.parametrize("dims,C", [((6, 5, 7), 4), ((9, 3, 4, 5), 3), ((40, 40, 12, 8), 20)])
+def test_device_sharded_cp_als_world1(group, oracle, dims, C):
+    """dmtk_gpu_cp_als_sharded with a library-owned NCCL communicator (world 1
+    here): every exchange point (MTTKRP partials, the last factor's column
+    norms and Gram, the fit's inner product, ||X||^2) runs as an NCCL
+    all-reduce inside the per-mode CUDA graphs; with one rank the result must
+    equal the single-GPU cp_als and the reference."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
+
+    x = oracle.gen_tensor(dims, 5)
+    t = dg.DenseTensor(dims, x)
+    comm = DeviceComm(0)
+    cfg = dg.AlsConfig(rank=C, max_iters=8, tol=0.0, seed=11)
+    res = dist_cp_als_device(t, comm, dims[-1], 0, cfg)
+    one = dg.cp_als(t, cfg)
+    want = [it.fit.fit for it in one.trace.iters]
+    assert len(res.fits) == len(want) == 8
+    assert np.max(np.abs(np.array(res.fits) - np.array(want))) <= 1e-12
+    for a, b in zip(res.factors, one.model.factors):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+    _, _, ref_fits, _ = oracle.cp_als(x, dims, C, 8, 0.0, 11)
+    assert np.max(np.abs(np.array(res.fits) - ref_fits)) <= 1e-9
+    comm.close()
+
+
+def test_device_sharded_cp_als_validation(group, oracle):
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
+
+    dims = (6, 5, 7)
+    t = dg.DenseTensor(dims, oracle.gen_tensor(dims, 5))
+    comm = DeviceComm(0)
+    with pytest.raises(RuntimeError, match="outside the global extent"):
+        dist_cp_als_device(t, comm, 7, 3, dg.AlsConfig(rank=2, max_iters=2, tol=0.0))
+    with pytest.raises(RuntimeError, match="per-mode sweep"):
+        dist_cp_als_device(t, comm, 7, 0, dg.AlsConfig(rank=2, max_iters=2, tol=0.0, dimension_tree=True))
+    comm.close()
