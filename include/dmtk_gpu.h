@@ -67,7 +67,10 @@ int dmtk_gpu_device_count(int* count);
  * Shape::Shape (shape.cpp:8-25). */
 int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const double* host, dmtk_gpu_tensor* out);
 /* Wrap an existing device buffer without copying (DenseTensor::borrow,
- * tensor.hpp:23); the caller keeps it alive and unchanged. */
+ * tensor.hpp:23); the caller keeps it alive and unchanged. The call waits for
+ * the device to finish pending work (the values are read later on the
+ * library's own stream, so writes still queued on the caller's streams must
+ * have landed). */
 int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double* device_ptr, dmtk_gpu_tensor* out);
 int dmtk_gpu_tensor_free(dmtk_gpu_tensor t);
 /* Shape-only view of a tensor handle (read back the device pointer). */

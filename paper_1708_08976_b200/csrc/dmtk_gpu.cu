@@ -1503,6 +1503,11 @@ int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double
         auto d = checked_dims(ndim, dims);
         if (!device_ptr) fail(DMTK_GPU_EINVAL, "DenseTensor: null data");
         context(device);
+        // the borrowed values must be final now (the library reads them on its
+        // own stream): wait for every pending write on the device, e.g. the
+        // caller's generator kernels still queued on another stream
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceSynchronize());
         auto t = std::make_unique<dmtk_gpu_tensor_s>();
         t->device = device;
         t->dims = d;

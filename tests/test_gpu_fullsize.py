@@ -112,6 +112,7 @@ def fmri_tensor(dims, seed=1):
 def test_cp_als_fmri_full_size_sweeps_agree():
     dims = (100, 100, 1200, 80)
     x = fmri_tensor(dims)
+    # (wrap waits for the generator kernels: cp_als reads x on the library's stream)
     t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
     fits = {}
     for name, tree, sym in (("per_mode", False, False), ("tree", True, False), ("sym", True, True)):
