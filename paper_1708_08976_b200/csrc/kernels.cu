@@ -35,15 +35,37 @@ __global__ void __launch_bounds__(256) krp_level_kernel(const double* __restrict
     const long long nch = (JC + kKrpChunk - 1) / kKrpChunk;
     const long long units = Q * nch;
     const int step = (2 * blockDim.x) % C;  // column advance per 2*blockDim entries
-    // 16-byte vectors when U, out and every block start are 16-byte aligned
-    const bool vec = (JC & 1) == 0 && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const int step4 = (4 * blockDim.x) % C;
+    // 32-byte vectors (sm_100 256-bit LDG/STG) when C is a multiple of 4 (no
+    // column wrap inside a vector) and U, out and every block start are
+    // 32-byte aligned (200^3 C=16: 0.81 -> 0.84 of the HBM roofline; with a
+    // wrap, C = 25, they measured 6% slower), else 16-byte ones
+    const uintptr_t al = reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(out);
+    const bool vec4 = (C & 3) == 0 && (al & 31) == 0;
+    const bool vec = (JC & 1) == 0 && (al & 15) == 0;
     for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
         const long long q = unit / nch;
         const long long f0 = (unit - q * nch) * kKrpChunk;
         const long long f1 = f0 + kKrpChunk < JC ? f0 + kKrpChunk : JC;
         const double* __restrict__ Pq = P + q * C;
         double* o = out + q * JC;
-        if (vec) {
+        if (vec4) {
+            const long long fs = f0 + 4 * threadIdx.x;
+            int c = static_cast<int>(fs % C);
+            for (long long f = fs; f < f1; f += 4 * blockDim.x) {
+                double u0, u1, u2, u3;
+                asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                             : "=d"(u0), "=d"(u1), "=d"(u2), "=d"(u3)
+                             : "l"(U + f));
+                const double v0 = __ldg(Pq + c) * u0, v1 = __ldg(Pq + c + 1) * u1;
+                const double v2 = __ldg(Pq + c + 2) * u2, v3 = __ldg(Pq + c + 3) * u3;
+                asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o + f), "d"(v0), "d"(v1), "d"(v2),
+                             "d"(v3)
+                             : "memory");
+                c += step4;
+                if (c >= C) c -= C;
+            }
+        } else if (vec) {
             const long long fs = f0 + 2 * threadIdx.x;
             int c = static_cast<int>(fs % C);
             for (long long f = fs; f < f1; f += 2 * blockDim.x) {
