@@ -12,6 +12,7 @@ import subprocess
 import sys
 
 import pytest
+import numpy as np
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -185,3 +186,20 @@ def test_tune_cache_file(tmp_path):
         assert "failures: 0" in r.stdout
     lines = cache.read_text().split("\n")
     assert len([l for l in lines if l.strip()]) >= 4  # boundary modes of both shapes + interior orders
+
+
+def test_measured_selection_random_shapes():
+    """Seeded random shapes (3- to 5-way, odd and even extents, ranks 1-40)
+    through the timed view selection (threshold lowered to 0), every mode and
+    algorithm against numpy."""
+    rng = np.random.default_rng(2024)
+    shapes = []
+    for _ in range(14):
+        n = int(rng.integers(3, 6))
+        dims = [int(rng.integers(2, 40 if n == 3 else 14)) for _ in range(n)]
+        shapes.append("x".join(map(str, dims)) + ":" + str(int(rng.integers(1, 41))))
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
