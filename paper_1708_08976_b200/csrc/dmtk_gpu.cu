@@ -719,7 +719,11 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         // krp.cpp:53-88), materialised once so a builder's head is one row load
         mp.tc.htab = nullptr;
         mp.tc.hrows = 0;
-        if (bgen.nf >= 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0) {
+        if (bgen.nf == 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu == C) {
+            // one slower factor: the head table is that factor itself (no copy)
+            mp.tc.htab = bgen.U[1];
+            mp.tc.hrows = bgen.ext[1];
+        } else if (bgen.nf >= 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0) {
             std::vector<const double*> in;
             std::vector<long long> rows;
             long long hr = 1;
