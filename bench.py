@@ -461,7 +461,16 @@ def main():
         rsh = dist_cp_als_device(tf, comm, glast, lo, dg.AlsConfig(rank=20, max_iters=25, tol=0.0, seed=1))
         wall = time.perf_counter() - t0
         its = sorted(1e3 * v for v in rsh.iter_seconds)
-        mx = torch.tensor([its[len(its) // 2], wall], dtype=torch.float64)
+        # the same over the dimension tree (two tensor passes per iteration)
+        cfg_t = lambda n: dg.AlsConfig(rank=20, max_iters=n, tol=0.0, seed=1, dimension_tree=True)  # noqa: E731
+        dist_cp_als_device(tf, comm, glast, lo, cfg_t(2))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t1 = time.perf_counter()
+        rtr = dist_cp_als_device(tf, comm, glast, lo, cfg_t(25))
+        wall_t = time.perf_counter() - t1
+        itt = sorted(1e3 * v for v in rtr.iter_seconds)
+        mx = torch.tensor([its[len(its) // 2], wall, itt[len(itt) // 2], wall_t], dtype=torch.float64)
         if world > 1:
             mx = mx.to(dev)
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)  # the slowest rank sets the job's time
@@ -471,6 +480,11 @@ def main():
                "iter_ms_median": round(float(mx[0]), 3), "wall_s": round(float(mx[1]), 4),
                "final_fit": rsh.fits[-1], "scaling": "weak", "ranks": world,
                "roofline_iter_ms": round(4 * 8.0 * nf / world / (hbm_peak * 1e9) * 1e3, 3),
+               "dimension_tree": {"iter_ms_median": round(float(mx[2]), 3), "wall_s": round(float(mx[3]), 4),
+                                  "final_fit": rtr.fits[-1],
+                                  "max_fit_diff_vs_per_mode": float(max(abs(a - b) for a, b in
+                                                                        zip(rsh.fits, rtr.fits))),
+                                  "roofline_iter_ms": round(2 * 8.0 * nf / world / (hbm_peak * 1e9) * 1e3, 3)},
                "path": "dmtk_gpu_cp_als_sharded: per-mode sweep on the device, NCCL all-reduces of the "
                        "I_n x C partials, the last factor's column norms and Gram and the fit inside the "
                        "per-mode CUDA graphs",

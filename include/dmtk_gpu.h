@@ -180,8 +180,10 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
  * other step runs redundantly and identically on every rank. Initialisation
  * follows KruskalModel::random (cp_als.cpp:87-99) over the global shape, each
  * rank keeping its rows of the last factor. factors_out: modes 0..N-2 in full,
- * then this rank's rows of mode N-1. The per-mode sweep only (dimtree = 0, an
- * unpacked tensor).
+ * then this rank's rows of mode N-1. The per-mode sweep, or with dimtree = 1
+ * the dimension tree (the left partial and the right half's non-last-mode
+ * multi-TTVs all-reduced; the split chosen on the global shape); not for a
+ * packed symmetric tensor.
  *
  * dmtk_gpu_comm_unique_id: 128-byte NCCL id, made on one rank and broadcast
  * by the caller (e.g. torch.distributed) to all ranks, which then call

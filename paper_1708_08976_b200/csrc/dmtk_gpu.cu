@@ -2036,8 +2036,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             fail(DMTK_GPU_EINVAL,
                  "mttkrp_two_step: mode 0 is a boundary mode with a degenerate partial KRP; use one_step instead");
         const int C = static_cast<int>(cfg->rank);
-        if (sh && (cfg->dimtree || t->sym01))
-            fail(DMTK_GPU_EINVAL, "cp_als_sharded: only the per-mode sweep on an unpacked slab is sharded");
+        if (sh && t->sym01) fail(DMTK_GPU_EINVAL, "cp_als_sharded: a packed symmetric slab is not supported");
         if (sh && (sh->last_lo < 0 || sh->last_lo + t->dims[N - 1] > sh->last_extent))
             fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab's last-mode rows lie outside the global extent");
         Context& ctx = context(t->device);
@@ -2167,15 +2166,18 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         int hsplit = 0;
         DevBuf Pbuf;
         if (tree) {
+            // (sharded: the split of the global shape, the same on every rank)
+            std::vector<long long> gd = t->pdims;
+            if (sh) gd[N - 1] = sh->last_extent;
             long long best = -1;
             for (int h = 1; h < N; ++h) {
-                const long long m = std::max(prod(t->pdims, 0, h), prod(t->pdims, h, N));
+                const long long m = std::max(prod(gd, 0, h), prod(gd, h, N));
                 if (best < 0 || m < best) {
                     best = m;
                     hsplit = h;
                 }
             }
-            Pbuf.ensure(static_cast<size_t>(best * C));
+            Pbuf.ensure(static_cast<size_t>(std::max(prod(t->pdims, 0, hsplit), prod(t->pdims, hsplit, N)) * C));
         }
         const long long rowsL = tree ? prod(t->pdims, 0, hsplit) : 0, rowsR = tree ? prod(t->pdims, hsplit, N) : 0;
         // left partial: every left row against the right half's KRP (M-major,
@@ -2186,6 +2188,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             const KrpGen bg = make_gen(t->pdims, hsplit, N, Uc.data(), C, ctx.ones.p);
             const KrpGen sg = make_gen(t->pdims, 0, 0, Uc.data(), C, ctx.ones.p);
             enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
+            shard_allreduce(sh, Pbuf.p, rowsL * C, s);  // sharded: the left partial summed over the slabs
         };
         auto pass_right = [&]() {
             const ModePlan mp = plan_view(rowsL, rowsR, 1, C, kTcKJ, 0, ctx.sms);
@@ -2193,10 +2196,19 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             const KrpGen sg = make_gen(t->pdims, N, N, Uc.data(), C, ctx.ones.p);
             enqueue_planned(*t, ctx, mp, kTcKJ, bg, sg, t->d, C, (300 + hsplit) * 128 + 1, -1, Pbuf.p, s, nullptr);
         };
+        // sharded: the right half's partial has this rank's last-mode rows, so a
+        // right mode other than the last sums its multi-TTV over the ranks, and the
+        // last mode updates its own rows (norms and Gram over the ranks)
+        auto upd = [&](int k, const double* Mn) {
+            if (sh && k == N - 1)
+                als_upd_sharded_last(k, Mn);
+            else
+                als_upd(k, Mn);
+        };
         // mode k of the half [lo, hi) from its partial (multi-TTV)
         auto half_step = [&](int k, int lo, int hi) {
             if (hi - lo == 1) {
-                als_upd(k, Pbuf.p);
+                upd(k, Pbuf.p);
                 return;
             }
             const std::vector<long long>& hd = t->sym01 ? t->dims : t->pdims;  // modes >= 2 are unpadded
@@ -2207,7 +2219,8 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
             count_launch(1);
             check_launch("multittv");
-            als_upd(k, M.p);
+            if (sh && lo == hsplit && k < N - 1) shard_allreduce(sh, M.p, dt * C, s);
+            upd(k, M.p);
         };
         struct Step {
             std::function<void()> fn;

@@ -84,6 +84,36 @@ def test_device_sharded_cp_als_validation(group, oracle):
     comm = DeviceComm(0)
     with pytest.raises(RuntimeError, match="outside the global extent"):
         dist_cp_als_device(t, comm, 7, 3, dg.AlsConfig(rank=2, max_iters=2, tol=0.0))
-    with pytest.raises(RuntimeError, match="per-mode sweep"):
-        dist_cp_als_device(t, comm, 7, 0, dg.AlsConfig(rank=2, max_iters=2, tol=0.0, dimension_tree=True))
+    with pytest.raises(RuntimeError, match="packed symmetric"):
+        dist_cp_als_device(_sym_slab(dg, oracle), comm, 6, 0,
+                           dg.AlsConfig(rank=2, max_iters=2, tol=0.0, dimension_tree=True))
+    comm.close()
+
+
+def _sym_slab(dg, oracle):
+    dims = (4, 4, 3, 6)
+    x = oracle.gen_tensor(dims, 9).reshape(dims[::-1])
+    x = x + np.swapaxes(x, -1, -2)  # symmetric in modes 0 and 1
+    return dg.DenseTensor(dims, np.ascontiguousarray(x).reshape(-1)).pack_symmetric01()
+
+
+@pytest.mark.parametrize("dims,C", [((9, 3, 4, 5), 3), ((40, 40, 12, 8), 20), ((6, 5, 7, 4, 3), 4)])
+def test_device_sharded_cp_als_dimension_tree_world1(group, oracle, dims, C):
+    """The dimension-tree sweep over last-mode shards (left partial all-reduced,
+    right-half multi-TTVs of the non-last modes all-reduced, the last factor's
+    rows local): with one rank, equal to the single-GPU tree and within 1e-9 of
+    the reference's per-mode fits."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
+
+    x = oracle.gen_tensor(dims, 5)
+    t = dg.DenseTensor(dims, x)
+    comm = DeviceComm(0)
+    cfg = dg.AlsConfig(rank=C, max_iters=6, tol=0.0, seed=11, dimension_tree=True)
+    res = dist_cp_als_device(t, comm, dims[-1], 0, cfg)
+    one = dg.cp_als(t, cfg)
+    want = [it.fit.fit for it in one.trace.iters]
+    assert np.max(np.abs(np.array(res.fits) - np.array(want))) <= 1e-12
+    _, _, ref_fits, _ = oracle.cp_als(x, dims, C, 6, 0.0, 11)
+    assert np.max(np.abs(np.array(res.fits) - ref_fits)) <= 1e-9
     comm.close()
