@@ -182,8 +182,9 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
  * rank keeping its rows of the last factor. factors_out: modes 0..N-2 in full,
  * then this rank's rows of mode N-1. The per-mode sweep, or with dimtree = 1
  * the dimension tree (the left partial and the right half's non-last-mode
- * multi-TTVs all-reduced; the split chosen on the global shape); not for a
- * packed symmetric tensor.
+ * multi-TTVs all-reduced; the split chosen on the global shape); a packed
+ * symmetric slab (dmtk_gpu_tensor_pack_sym01 of this rank's slab) runs its
+ * pair-index tree with Q all-reduced.
  *
  * dmtk_gpu_comm_unique_id: 128-byte NCCL id, made on one rank and broadcast
  * by the caller (e.g. torch.distributed) to all ranks, which then call

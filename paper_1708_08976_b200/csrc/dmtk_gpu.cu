@@ -2036,7 +2036,6 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             fail(DMTK_GPU_EINVAL,
                  "mttkrp_two_step: mode 0 is a boundary mode with a degenerate partial KRP; use one_step instead");
         const int C = static_cast<int>(cfg->rank);
-        if (sh && t->sym01) fail(DMTK_GPU_EINVAL, "cp_als_sharded: a packed symmetric slab is not supported");
         if (sh && (sh->last_lo < 0 || sh->last_lo + t->dims[N - 1] > sh->last_extent))
             fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab's last-mode rows lie outside the global extent");
         Context& ctx = context(t->device);
@@ -2219,7 +2218,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
             count_launch(1);
             check_launch("multittv");
-            if (sh && lo == hsplit && k < N - 1) shard_allreduce(sh, M.p, dt * C, s);
+            if (sh && lo > 0 && k < N - 1) shard_allreduce(sh, M.p, dt * C, s);  // a right-half mode
             upd(k, M.p);
         };
         struct Step {
@@ -2247,6 +2246,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
                 const KrpGen bg = make_gen(t->pdims, 1, Np, pk_ptrs.data(), C, ctx.ones.p);
                 const KrpGen sg = make_gen(t->pdims, 0, 0, pk_ptrs.data(), C, ctx.ones.p);
                 enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, 400 * 128, -1, Qb.p, s, nullptr);
+                shard_allreduce(sh, Qb.p, sPp * C, s);  // sharded: Q summed over the slabs
             };
             auto sym_mode = [&](int k) {  // mode 0 (with U_1) or mode 1 (with the new U_0)
                 launch_sym01_mttv(Qb.p, sI, C, k == 0 ? Um[1] : Um[0], M.p, s);

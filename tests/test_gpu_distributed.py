@@ -84,9 +84,6 @@ def test_device_sharded_cp_als_validation(group, oracle):
     comm = DeviceComm(0)
     with pytest.raises(RuntimeError, match="outside the global extent"):
         dist_cp_als_device(t, comm, 7, 3, dg.AlsConfig(rank=2, max_iters=2, tol=0.0))
-    with pytest.raises(RuntimeError, match="packed symmetric"):
-        dist_cp_als_device(_sym_slab(dg, oracle), comm, 6, 0,
-                           dg.AlsConfig(rank=2, max_iters=2, tol=0.0, dimension_tree=True))
     comm.close()
 
 
@@ -116,4 +113,21 @@ def test_device_sharded_cp_als_dimension_tree_world1(group, oracle, dims, C):
     assert np.max(np.abs(np.array(res.fits) - np.array(want))) <= 1e-12
     _, _, ref_fits, _ = oracle.cp_als(x, dims, C, 6, 0.0, 11)
     assert np.max(np.abs(np.array(res.fits) - ref_fits)) <= 1e-9
+    comm.close()
+
+
+def test_device_sharded_cp_als_symmetric_packed_world1(group, oracle):
+    """A packed symmetric slab (modes 0/1): Q over the pair index all-reduced,
+    the right half as in the tree; with one rank equal to the single-GPU
+    packed sweep."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
+
+    tp = _sym_slab(dg, oracle)
+    comm = DeviceComm(0)
+    cfg = dg.AlsConfig(rank=3, max_iters=6, tol=0.0, seed=11)
+    res = dist_cp_als_device(tp, comm, 6, 0, cfg)
+    one = dg.cp_als(tp, cfg)
+    want = [it.fit.fit for it in one.trace.iters]
+    assert np.max(np.abs(np.array(res.fits) - np.array(want))) <= 1e-12
     comm.close()
