@@ -597,6 +597,71 @@ __global__ void __launch_bounds__(256) als_solve_kernel(const double* __restrict
     if (tid == 0) flag[0] = 1;
 }
 
+// The same solve as als_solve_kernel by in-place Gauss-Jordan inversion: n
+// elimination steps, each one reciprocal and one FMA per entry with every
+// entry of the step independent, so the serial chain is n x (pivot load,
+// reciprocal, FMA) instead of the Cholesky pivot sequence followed by the
+// column substitutions. No pivoting: H is symmetric positive definite, and the
+// pivot of step k is the Schur-complement diagonal that the Cholesky
+// factorisation takes its square root of, so the same 1e-12 * trace test
+// sends singular systems to the Jacobi fallback (flag 0). Entries are
+// double-buffered in shared memory (one barrier per step).
+__global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restrict__ grams, int nmodes, int skip,
+                                                           int n, double* __restrict__ Hout,
+                                                           double* __restrict__ Hinv, int* __restrict__ flag) {
+    constexpr int LDA = 33;
+    __shared__ double A[2][32 * LDA];
+    __shared__ double s_tr;
+    const int tid = threadIdx.x;
+    const int nn = n * n;
+    for (int e = tid; e < nn; e += blockDim.x) {
+        double h = 1.0;
+        for (int k = 0; k < nmodes; ++k)
+            if (k != skip) h *= grams[static_cast<long long>(k) * nn + e];
+        Hout[e] = h;
+        const int i = e / n, j = e - (e / n) * n;
+        A[0][i * LDA + j] = h;
+    }
+    __syncthreads();
+    if (tid < 32) {  // trace by a shuffle tree (four short chains, not one of n)
+        double v = tid < n ? A[0][tid * LDA + tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tid == 0) s_tr = v;
+    }
+    __syncthreads();
+    const double tol = 1e-12 * s_tr;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        const double* a = A[k & 1];
+        double* b = A[(k + 1) & 1];
+        const double p = a[k * LDA + k];
+        if (p <= tol) {  // uniform across the CTA: every thread reads the same pivot
+            if (tid == 0) flag[0] = 0;
+            return;
+        }
+        const double r = 1.0 / p;
+        for (int e = tid; e < nn; e += blockDim.x) {
+            const int i = e / n, j = e - (e / n) * n;
+            double v;
+            if (i == k)
+                v = j == k ? r : a[k * LDA + j] * r;
+            else if (j == k)
+                v = -a[i * LDA + k] * r;
+            else
+                v = fma(-a[i * LDA + k] * r, a[k * LDA + j], a[i * LDA + j]);
+            b[i * LDA + j] = v;
+        }
+        __syncthreads();
+    }
+    const double* a = A[n & 1];
+    for (int e = tid; e < nn; e += blockDim.x) {
+        const int i = e / n, j = e - (e / n) * n;
+        Hinv[e] = 0.5 * (a[i * LDA + j] + a[j * LDA + i]);  // symmetric to the last bit
+    }
+    if (tid == 0) flag[0] = 1;
+}
+
 // U = M H^-1, one output element per thread (H^-1 staged in shared memory).
 __global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, const double* __restrict__ M,
                                      long long rows, double* __restrict__ U, const int* __restrict__ flag) {
@@ -1137,7 +1202,11 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         double* Hinv = scratch;
         double* V = scratch + 64 * 64;
         double* gain = V + 64 * 64;
-        als_solve_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
+        static const bool chol = std::getenv("DMTK_GPU_ALS_CHOL_INVERSE") != nullptr;
+        if (chol)
+            als_solve_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
+        else
+            als_solve_gj_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
         const long long tot = rows * C;
         apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, C * C * 8, s>>>(Hinv, C, M, rows, U,
                                                                                             flag);
