@@ -104,16 +104,29 @@ __global__ void __launch_bounds__(256) multittv_partial_kernel(const double* __r
     const int parts = blockDim.x / C;
     const int p = threadIdx.x / C;
     const int c = threadIdx.x - p * C;
-    double acc = 0.0;
+    // four independent chains (term u of a thread goes to chain u mod 4),
+    // combined in a fixed order: B200's FP64 add latency is ~100 cycles
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (p < parts) {
-        for (long long tau = t0 + p; tau < t1; tau += parts) {
+        long long tau = t0 + p;
+        for (; tau + 3 * parts < t1; tau += 4 * parts) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long tu = tau + u * parts;
+                const long long b = div_nn(tu, A);
+                const long long a = tu - b * A;
+                const long long row = a + A * (i + dt * b);
+                acc[u] += P[row * C + c] * krp_value(kl, a, c) * krp_value(kr, b, c);
+            }
+        }
+        for (int u = 0; tau < t1; tau += parts, ++u) {
             const long long b = div_nn(tau, A);
             const long long a = tau - b * A;
             const long long row = a + A * (i + dt * b);
-            acc += P[row * C + c] * krp_value(kl, a, c) * krp_value(kr, b, c);
+            acc[u] += P[row * C + c] * krp_value(kl, a, c) * krp_value(kr, b, c);
         }
     }
-    red[threadIdx.x] = acc;
+    red[threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     __syncthreads();
     if (threadIdx.x < C) {
         double t = 0.0;
@@ -1072,18 +1085,22 @@ void launch_sym01_pairs(const double* A, const double* B, long long I, int C, lo
     sym01_pairs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(A, B, I, C, Pp, W);
 }
 
-long long multittv_ws_doubles(long long A, long long dt, long long B, int C) {
+// chunks per output row: about eight 256-thread blocks per SM in all, each
+// thread left with at least a few terms per chain
+static long long multittv_chunks(long long A, long long dt, long long B) {
     const long long T = A * B;
-    long long S = (2 * 148 + dt - 1) / dt;
-    S = std::max<long long>(1, std::min<long long>(S, std::max<long long>(1, T / 32)));
-    return S * dt * C;
+    long long S = (8 * 148 + dt - 1) / dt;
+    return std::max<long long>(1, std::min<long long>(S, std::max<long long>(1, T / 32)));
+}
+
+long long multittv_ws_doubles(long long A, long long dt, long long B, int C) {
+    return multittv_chunks(A, dt, B) * dt * C;
 }
 
 void launch_multittv(const double* P, int C, long long A, long long dt, long long B, const KrpGen& kl,
                      const KrpGen& kr, double* ws, double* M, cudaStream_t s) {
     const long long T = A * B;
-    long long S = (2 * 148 + dt - 1) / dt;
-    S = std::max<long long>(1, std::min<long long>(S, std::max<long long>(1, T / 32)));
+    const long long S = multittv_chunks(A, dt, B);
     const long long per = (T + S - 1) / S;
     multittv_partial_kernel<<<dim3(static_cast<unsigned>(dt), static_cast<unsigned>(S)), 256, 0, s>>>(
         P, C, A, dt, B, kl, kr, per, ws);
