@@ -66,6 +66,12 @@ int dmtk_gpu_device_count(int* count);
 /* Upload a host tensor (natural order) to `device`. Validates the shape like
  * Shape::Shape (shape.cpp:8-25). */
 int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const double* host, dmtk_gpu_tensor* out);
+/* dmtk::gen_tensor (bench.cpp:88-97, bench.hpp:22) generated in HBM: dist 0 =
+ * Dist::uniform, the same mt19937_64(seed) draws in the same order, bitwise
+ * (the stream is split across CTAs by characteristic-polynomial jump-ahead);
+ * dist 1 = Dist::ones. Same layout as dmtk_gpu_tensor_upload. SURVEY 8f-3. */
+int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t seed, int dist,
+                             dmtk_gpu_tensor* out);
 /* Wrap an existing device buffer without copying (DenseTensor::borrow,
  * tensor.hpp:23); the caller keeps it alive and unchanged. The call waits for
  * the device to finish pending work (the values are read later on the

@@ -124,6 +124,18 @@ class DenseTensor:
         t._handle = h
         return t
 
+    @classmethod
+    def generate(cls, dims: Sequence[int], seed: int, dist: str = "uniform", device: int = 0) -> "DenseTensor":
+        """dmtk::gen_tensor (bench.cpp:88-97) generated in HBM: the reference's
+        mt19937_64(seed) uniform(0,1) draws bitwise, or Dist::ones."""
+        if dist not in ("uniform", "ones"):
+            raise InvalidArgument("gen_tensor: unknown distribution")
+        t = cls(dims, None, device)
+        d = _i64(t.dims)
+        _check(lib.dmtk_gpu_tensor_generate(device, len(d), d.ctypes.data_as(_lib.i64p), C.c_uint64(seed),
+                                            0 if dist == "uniform" else 1, C.byref(t._handle)))
+        return t
+
     def pack_symmetric01(self) -> "DenseTensor":
         """A packed copy of a tensor symmetric in modes 0 and 1 (upper triangle
         of every slice; dmtk_gpu_tensor_pack_sym01). Supports cp_als (a

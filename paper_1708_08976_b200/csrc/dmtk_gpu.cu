@@ -1502,6 +1502,52 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
     });
 }
 
+int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t seed, int dist,
+                             dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        auto d = checked_dims(ndim, dims);
+        if (!out) fail(DMTK_GPU_EINVAL, "gen_tensor: null output");
+        if (dist != 0 && dist != 1) fail(DMTK_GPU_EINVAL, "gen_tensor: unknown distribution");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        auto t = std::make_unique<dmtk_gpu_tensor_s>();
+        t->device = device;
+        t->dims = d;
+        t->total = prod(d, 0, ndim);
+        t->pdims = d;
+        if (ndim > 0 && d[0] % 2 != 0 && t->total > 0) t->pdims[0] = d[0] + 1;  // same layout as an upload
+        t->ptotal = prod(t->pdims, 0, ndim);
+        double* p = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(std::max<long long>(t->ptotal, 1)) *
+                                                             sizeof(double),
+                           ctx.stream));
+        t->d = p;
+        t->owned = true;
+        if (t->pdims != t->dims) CK(cudaMemsetAsync(p, 0, static_cast<size_t>(t->ptotal) * sizeof(double), ctx.stream));
+        if (t->total > 0) {
+            if (dist == 1) {
+                if (t->pdims == t->dims) {
+                    launch_fill(p, t->total, 1.0, ctx.stream);
+                } else {  // ones in the logical slices, the pad slice stays zero
+                    launch_fill(p, t->ptotal, 1.0, ctx.stream);
+                    CK(cudaMemset2DAsync(p + d[0], static_cast<size_t>(t->pdims[0]) * sizeof(double), 0, sizeof(double),
+                                         static_cast<size_t>(t->total / d[0]), ctx.stream));
+                }
+            } else {
+                uint64_t* scratch = nullptr;
+                CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), dmtkg::mt64_scratch_words(ctx.sms) * 8,
+                                   ctx.stream));
+                dmtkg::mt64_generate(p, t->total, d[0], t->pdims[0], seed, ctx.sms, scratch, ctx.stream);
+                CK(cudaGetLastError());
+                CK(cudaFreeAsync(scratch, ctx.stream));
+            }
+        }
+        CK(cudaStreamSynchronize(ctx.stream));
+        *out = t.release();
+    });
+}
+
 int dmtk_gpu_tensor_wrap(int device, int ndim, const int64_t* dims, const double* device_ptr, dmtk_gpu_tensor* out) {
     return guarded([&] {
         auto d = checked_dims(ndim, dims);

@@ -53,6 +53,10 @@ void launch_fit(const double* U, const double* Mlast, long long rows, int C, con
                 const double* normx, double* out, cudaStream_t s);
 void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s);
 void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
+// mt_gen.cu: gen_tensor (bench.cpp:88-97) on the device, bitwise; dst[(q / d0) * pd0 + q % d0] = draw q
+size_t mt64_scratch_words(int nsm);
+void mt64_generate(double* dst, long long n, long long d0, long long pd0, uint64_t seed, int nsm,
+                   uint64_t* dev_scratch, cudaStream_t s);
 // CP-ALS with cached Grams
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
