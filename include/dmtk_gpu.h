@@ -72,6 +72,10 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
  * dist 1 = Dist::ones. Same layout as dmtk_gpu_tensor_upload. SURVEY 8f-3. */
 int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t seed, int dist,
                              dmtk_gpu_tensor* out);
+/* Host-side check of the generator's jump-ahead (no device needed): raw
+ * (untempered) words 312+start .. 623+start of mt19937_64(seed), i.e. the
+ * words whose tempered values are draws start .. start+311. 0 or -1. */
+int dmtk_gpu_mt64_jump(uint64_t seed, int64_t start, uint64_t* words312);
 /* Wrap an existing device buffer without copying (DenseTensor::borrow,
  * tensor.hpp:23); the caller keeps it alive and unchanged. The call waits for
  * the device to finish pending work (the values are read later on the

@@ -290,3 +290,31 @@ void mt64_generate(double* dst, long long n, long long d0, long long pd0, uint64
 size_t mt64_scratch_words(int nsm) { return static_cast<size_t>(kRaw + 1) + static_cast<size_t>(nsm) * kPW; }
 
 }  // namespace dmtkg
+
+// Host-side check of the jump-ahead (no device needed): the raw words
+// x_{312+start} .. x_{623+start} of mt19937_64(seed), formed from the first
+// raw words and x^(311+start) mod phi exactly as a generator CTA forms its
+// window. Returns 0, or -1 on a negative start.
+extern "C" int dmtk_gpu_mt64_jump(uint64_t seed, int64_t start, uint64_t* words312) {
+    using namespace dmtkg;
+    if (start < 0 || !words312) return -1;
+    try {
+        const auto raw = raw_words(seed, kRaw + 1);
+        const Poly r = start == 0 ? monomial(kNN - 1) : mulmod(monomial(kNN - 1), xpow(start));
+        for (int k = 0; k < kNN; ++k) {
+            uint64_t acc = 0;
+            for (int w = 0; w < kPW; ++w) {
+                uint64_t c = r[w];
+                while (c) {
+                    const int b = __builtin_ctzll(c);
+                    c &= c - 1;
+                    acc ^= raw[1 + 64 * w + b + k];
+                }
+            }
+            words312[k] = acc;
+        }
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
