@@ -51,7 +51,13 @@ __device__ inline double mt_value(uint64_t y) {
     y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
     y ^= (y << 37) & 0xFFF7EEE000000000ULL;
     y ^= y >> 43;
-    return static_cast<double>(y >> 11) * 0x1.0p-53;
+    // (y >> 11) * 2^-53 built from integer ops (exact: m < 2^53), keeping the
+    // FP64 pipe's ~100-cycle conversion and multiply latency off each step
+    const uint64_t m = y >> 11;
+    if (m == 0) return 0.0;
+    const int e = 63 - __clzll(static_cast<long long>(m));  // 0..52
+    return __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(e + 970) << 52) |
+                                                       ((m << (52 - e)) & 0xFFFFFFFFFFFFFULL)));
 }
 
 // raw words x_0 .. x_{count-1} of mt19937_64(seed) (x_0..x_311 = the seeded state)
@@ -245,15 +251,17 @@ __global__ void __launch_bounds__(kNN) mt64_generate_kernel(const uint64_t* __re
     long long q = start + tid;
     long long row = q / d0, col = q - (q / d0) * d0;
     for (int b = 0;; ++b) {
+        double v = 0.0;
         if (act) {
             const uint64_t* old = ring + (b % 3) * kMM;
             const uint64_t* nxt = ring + ((b + 1) % 3) * kMM;
             const uint64_t x0 = old[tid];
             const uint64_t nw = mt_twist(x0, tid + 1 < kMM ? old[tid + 1] : nxt[0], nxt[tid]);
-            if (q < end) dst[row * pd0 + col] = mt_value(x0);
             ring[((b + 2) % 3) * kMM + tid] = nw;
+            v = mt_value(x0);
         }
         asm volatile("bar.sync 1, 160;" ::: "memory");
+        if (act && q < end) dst[row * pd0 + col] = v;  // after the barrier: tempering overlaps the wait
         if (start + static_cast<long long>(b + 1) * kMM >= end) break;
         q += kMM;
         col += kMM;
