@@ -217,14 +217,14 @@ std::vector<uint64_t> jump_coeffs(long long chunk, int P) {
 
 // One CTA per chunk: window from the staged raw words and r_p, then the
 // recurrence. Output q (tensor order) goes to dst[(q / d0) * pd0 + q % d0].
-__global__ void __launch_bounds__(kNN) mt64_generate_kernel(const uint64_t* __restrict__ raw,
+__global__ void __launch_bounds__(320) mt64_generate_kernel(const uint64_t* __restrict__ raw,
                                                             const uint64_t* __restrict__ coeffs, long long n,
                                                             long long chunk, long long d0, long long pd0,
                                                             double* __restrict__ dst) {
     extern __shared__ uint64_t sm[];
     uint64_t* sraw = sm;             // x_1 .. x_kRaw
     uint64_t* sco = sm + kRaw;       // r_p
-    uint64_t* ring = sco + kPW;      // three 156-word blocks
+    uint64_t* ring = sco + kPW;      // four 156-word blocks
     const int tid = threadIdx.x;
     const long long start = static_cast<long long>(blockIdx.x) * chunk;
     if (start >= n) return;
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kNN) mt64_generate_kernel(const uint64_t* __re
     for (int i = tid; i < kRaw; i += blockDim.x) sraw[i] = raw[i + 1];
     for (int i = tid; i < kPW; i += blockDim.x) sco[i] = coeffs[static_cast<long long>(blockIdx.x) * kPW + i];
     __syncthreads();
-    {  // word tid of the window: x_{312 + start + tid} = XOR_{r_i = 1} x_{1 + i + tid}
+    if (tid < kNN) {  // word tid of the window: x_{312 + start + tid} = XOR_{r_i = 1} x_{1 + i + tid}
         uint64_t acc = 0;
         for (int w = 0; w < kPW; ++w) {
             uint64_t c = sco[w];
@@ -245,36 +245,41 @@ __global__ void __launch_bounds__(kNN) mt64_generate_kernel(const uint64_t* __re
         ring[tid] = acc;  // blocks 0 and 1
     }
     __syncthreads();
-    if (tid >= 160) return;  // five warps carry on (a named barrier counts whole warps)
-    const bool act = tid < kMM;  // one thread per word of a 156-word block
-    // position of output start + tid in the (possibly padded) layout, advanced by 156 per step
-    long long q = start + tid;
-    long long row = q / d0, col = q - (q / d0) * d0;
-    for (int b = 0;; ++b) {
-        double v = 0.0;
-        if (act) {
-            const uint64_t* old = ring + (b % 3) * kMM;
-            const uint64_t* nxt = ring + ((b + 1) % 3) * kMM;
+    // Warp-specialised steps over a four-block ring: warps 0-4 run the
+    // recurrence (block b+2 from blocks b, b+1), warps 5-9 temper and store
+    // block b-1, which stays untouched until step b+1 overwrites its slot.
+    const long long nblk = (end - start + kMM - 1) / kMM;  // blocks this chunk outputs
+    const bool rec = tid < kMM;
+    const int u = tid - 160;
+    const bool sto = u >= 0 && u < kMM;
+    long long row = 0, col = 0, q = start + u;
+    if (sto) {
+        row = q / d0;
+        col = q - row * d0;
+    }
+    for (long long b = 0; b <= nblk; ++b) {
+        if (rec) {
+            const uint64_t* old = ring + (b & 3) * kMM;
+            const uint64_t* nxt = ring + ((b + 1) & 3) * kMM;
             const uint64_t x0 = old[tid];
-            const uint64_t nw = mt_twist(x0, tid + 1 < kMM ? old[tid + 1] : nxt[0], nxt[tid]);
-            ring[((b + 2) % 3) * kMM + tid] = nw;
-            v = mt_value(x0);
+            ring[((b + 2) & 3) * kMM + tid] = mt_twist(x0, tid + 1 < kMM ? old[tid + 1] : nxt[0], nxt[tid]);
+        } else if (sto && b > 0) {
+            const uint64_t y = ring[((b - 1) & 3) * kMM + u];
+            if (q < end) dst[row * pd0 + col] = mt_value(y);
+            q += kMM;
+            col += kMM;
+            while (col >= d0) {
+                col -= d0;
+                ++row;
+            }
         }
-        asm volatile("bar.sync 1, 160;" ::: "memory");
-        if (act && q < end) dst[row * pd0 + col] = v;  // after the barrier: tempering overlaps the wait
-        if (start + static_cast<long long>(b + 1) * kMM >= end) break;
-        q += kMM;
-        col += kMM;
-        while (col >= d0) {
-            col -= d0;
-            ++row;
-        }
+        __syncthreads();
     }
 }
 
 }  // namespace
 
-size_t mt64_generate_smem() { return static_cast<size_t>(kRaw + kPW + 3 * kMM) * sizeof(uint64_t); }
+size_t mt64_generate_smem() { return static_cast<size_t>(kRaw + kPW + 4 * kMM) * sizeof(uint64_t); }
 
 void mt64_generate(double* dst, long long n, long long d0, long long pd0, uint64_t seed, int nsm,
                    uint64_t* dev_scratch, cudaStream_t s) {
@@ -290,7 +295,7 @@ void mt64_generate(double* dst, long long n, long long d0, long long pd0, uint64
     cudaMemcpyAsync(dco, co.data(), co.size() * 8, cudaMemcpyHostToDevice, s);
     const size_t smem = mt64_generate_smem();
     cudaFuncSetAttribute(mt64_generate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    mt64_generate_kernel<<<P, kNN, smem, s>>>(draw, dco, n, chunk, d0, pd0, dst);
+    mt64_generate_kernel<<<P, 320, smem, s>>>(draw, dco, n, chunk, d0, pd0, dst);
     // the host vectors must outlive the async copies (pageable: the copies are
     // staged synchronously before cudaMemcpyAsync returns)
 }
