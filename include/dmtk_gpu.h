@@ -69,7 +69,22 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
 /* dmtk::gen_tensor (bench.cpp:88-97, bench.hpp:22) generated in HBM: dist 0 =
  * Dist::uniform, the same mt19937_64(seed) draws in the same order, bitwise
  * (the stream is split across CTAs by characteristic-polynomial jump-ahead);
- * dist 1 = Dist::ones. Same layout as dmtk_gpu_tensor_upload. SURVEY 8f-3. */
+ * dist 1 = Dist::ones. Same layout as dmtk_gpu_tensor_upload. SURVEY 8f-3.
+ * The BASELINE configs that are not U[0,1) are
+ * fixed transforms of the same uniforms u_0, u_1, ... (natural order):
+ *   DMTK_GPU_DIST_SIGNED    U[-1,1):  x_e = 2 u_e - 1
+ *   DMTK_GPU_DIST_NORMAL    N(0,1), Box-Muller on (u_2k, u_2k+1):
+ *                           x_2k = R cos(2 pi u_2k+1), x_2k+1 = R sin(2 pi u_2k+1),
+ *                           R = sqrt(-2 log(1 - u_2k))
+ *   DMTK_GPU_DIST_SYMSLICE  dims (I, I, rest...): every slice q symmetric with
+ *                           unit diagonal, X(i,j,q) = X(j,i,q) = tanh(0.3 z_m),
+ *                           z the N(0,1) stream above, m = q I(I-1)/2 + j(j-1)/2 + i
+ *                           for i < j (BASELINE config 5)
+ * computed with explicitly rounded IEEE operations so that a host restatement
+ * reproduces the bytes exactly. A factor matrix of gen_factors (bench.cpp:108-116)
+ * is the 1-way tensor {rows * rank} with seed mode_seed(seed, n). */
+enum { DMTK_GPU_DIST_UNIFORM = 0, DMTK_GPU_DIST_ONES = 1, DMTK_GPU_DIST_SIGNED = 2, DMTK_GPU_DIST_NORMAL = 3,
+       DMTK_GPU_DIST_SYMSLICE = 4 };
 int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t seed, int dist,
                              dmtk_gpu_tensor* out);
 /* Host-side check of the generator's jump-ahead (no device needed): raw
@@ -178,6 +193,22 @@ typedef struct {
 int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out,
                     double* fits_out, double* iter_seconds_out, double* mode_seconds_out, int* n_iters,
                     int* zero_tensor, double* tensor_norm_out);
+
+/* dmtk::als_iterate (cp_als.hpp:74-75, cp_als.cpp:122-158): one Gauss-Seidel
+ * sweep over modes 0..N-1 of the model (factors[k]: host row-major
+ * factor_rows[k] x factor_cols[k], updated in place; lambda: nlambda = rank,
+ * updated in place) against t, with ||X|| = norm_x supplied by the caller
+ * (cp_als passes tensor_norm). fit4_out = {fit, rel_residual, abs_residual,
+ * defined} of the reconstruction-free fit from the last mode;
+ * seconds_out (may be NULL) = the sweep's device time; mode_seconds_out (may
+ * be NULL) = ndim per-mode seconds. Uses cfg->algo / order / threads; the
+ * rank comes from the model. Validation follows validate_model
+ * (cp_als.cpp:74-83) then the MTTKRP checks. iter_index is the record's
+ * index (AlsIterRecord::iter) and does not change the computation. */
+int dmtk_gpu_als_iterate(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, int nfactors, double* const* factors,
+                         const int64_t* factor_rows, const int64_t* factor_cols, double* lambda, int64_t nlambda,
+                         double norm_x, int iter_index, double* fit4_out, double* seconds_out,
+                         double* mode_seconds_out);
 
 /* Multi-GPU CP-ALS over last-mode shards (the reference's
  * cp_als, cp_als.cpp:122-200, with the tensor split along its slowest mode).

@@ -261,6 +261,39 @@ inline AlsResult cp_als(const DenseTensor& x, const AlsConfig& config, bool dime
     return r;
 }
 
+/// dmtk::als_iterate (cp_als.hpp:74-75): one sweep of `model` in place.
+inline AlsIterRecord als_iterate(const DenseTensor& x, KruskalModel& model, const AlsConfig& config, double norm_x,
+                                 int iter_index) {
+    std::vector<double*> ptrs;
+    std::vector<std::int64_t> rows, cols;
+    for (auto& u : model.factors) {
+        ptrs.push_back(u.data());
+        rows.push_back(u.rows());
+        cols.push_back(u.cols());
+    }
+    if (cols.empty()) cols.push_back(0);
+    dmtk_gpu_als_config c{config.rank, config.max_iters, config.tol, config.seed, config.threads,
+                          static_cast<int>(config.algo), static_cast<int>(config.order), 0};
+    double f4[4] = {0, 0, 0, 0}, secs = 0;
+    std::vector<double> msecs(std::max<std::size_t>(model.factors.size(), 1));
+    check(dmtk_gpu_als_iterate(handle(x), &c, static_cast<int>(ptrs.size()), ptrs.data(), rows.data(), cols.data(),
+                               model.lambda.data(), static_cast<std::int64_t>(model.lambda.size()), norm_x,
+                               iter_index, f4, &secs, msecs.data()));
+    AlsIterRecord rec;
+    rec.iter = iter_index;
+    rec.fit.fit = f4[0];
+    rec.fit.rel_residual = f4[1];
+    rec.fit.abs_residual = f4[2];
+    rec.fit.defined = f4[3] != 0.0;
+    rec.total_seconds = secs;
+    for (std::size_t n = 0; n < model.factors.size(); ++n) {
+        TimeBreakdown t;
+        t.total = msecs[n];
+        rec.mode_time.push_back(t);
+    }
+    return rec;
+}
+
 /// dmtk::fit (cp_als.hpp:79)
 inline FitResult fit(const DenseTensor& x, const KruskalModel& model, int threads = 1) {
     std::vector<const double*> ptrs;

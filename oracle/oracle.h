@@ -53,6 +53,18 @@ void orc_gen_factors(int ndim, const int64_t* dims, int64_t rank, uint64_t seed,
 void orc_kruskal_random(int ndim, const int64_t* dims, int64_t rank, uint64_t seed,
                         double* factors_out, double* lambda_out);
 
+/* ---- seeded value distributions (BASELINE configs 3-5; see oracle.c):
+ * dist 0 U[0,1) (gen_tensor), 1 ones, 2 U[-1,1), 3 N(0,1) Box-Muller,
+ * 4 symmetric fMRI slices (unit diagonal, tanh(0.3 z) off-diagonal).
+ * Natural order, `threads` worker threads for the transform. 0 or -1. */
+int orc_gen_dist(uint64_t seed, int dist, int ndim, const int64_t* dims, int threads, double* out);
+/* uniform draws a distribution consumes */
+int64_t orc_dist_uniforms(int dist, int ndim, const int64_t* dims);
+/* gen_factors (bench.cpp:108-116) with the transform of `dist` per factor stream */
+int orc_gen_factors_dist(int ndim, const int64_t* dims, int64_t rank, uint64_t seed, int dist, double* out);
+double orc_box_muller(double u0, double u1, int second);
+double orc_tanh_portable(double y);
+
 /* ---- Khatri-Rao (oracle.cpp:9-36 krp_kron; krp.hpp:19-32 contract) -------
  * K = in[0] (.) in[1] (.) ... (.) in[Z-1], last input fastest, associated
  * left to right. out is (prod rows) x cols row-major. Returns 0 or -1. */

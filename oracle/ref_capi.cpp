@@ -247,6 +247,36 @@ int ref_cp_als(int ndim, const int64_t* dims, const double* x, int64_t rank, int
     });
 }
 
+// dmtk::als_iterate (cp_als.hpp:74-75): one sweep of `model` in place;
+// out4 = fit, rel, abs, defined; *seconds = total_seconds.
+int ref_als_iterate(int ndim, const int64_t* dims, const double* x, int64_t rank, double* factors, double* lambda,
+                    int threads, int algo, int order, double norm_x, int iter_index, double* out4, double* seconds) {
+    return guarded([&] {
+        const dmtk::Shape shape = shape_of(ndim, dims);
+        const dmtk::DenseTensor t = dmtk::DenseTensor::borrow(shape, x, shape.total());
+        dmtk::KruskalModel m;
+        m.factors = unpack(ndim, dims, rank, factors);
+        m.lambda.assign(lambda, lambda + rank);
+        dmtk::AlsConfig cfg;
+        cfg.rank = rank;
+        cfg.threads = threads;
+        cfg.algo = static_cast<dmtk::MttkrpAlgo>(algo);
+        cfg.order = static_cast<dmtk::TwoStepOrder>(order);
+        const dmtk::AlsIterRecord r = dmtk::als_iterate(t, m, cfg, norm_x, iter_index);
+        std::int64_t off = 0;
+        for (const auto& u : m.factors) {
+            std::memcpy(factors + off, u.data(), sizeof(double) * static_cast<size_t>(u.rows() * u.cols()));
+            off += u.rows() * u.cols();
+        }
+        std::memcpy(lambda, m.lambda.data(), sizeof(double) * m.lambda.size());
+        out4[0] = r.fit.fit;
+        out4[1] = r.fit.rel_residual;
+        out4[2] = r.fit.abs_residual;
+        out4[3] = r.fit.defined ? 1.0 : 0.0;
+        if (seconds) *seconds = r.total_seconds;
+    });
+}
+
 // dmtk::fit (cp_als.hpp:79): returns fit, rel, abs, defined.
 int ref_fit(int ndim, const int64_t* dims, const double* x, int64_t rank, const double* factors,
             const double* lambda, int threads, double* out4) {

@@ -6,6 +6,7 @@ the Python mirror of the reference interface over its C ABI. Importing it
 without the built library raises: there is no CPU fallback.
 """
 from .api import (  # noqa: F401
+    DISTS,
     AlsConfig,
     AlsIterRecord,
     AlsResult,
@@ -23,12 +24,14 @@ from .api import (  # noqa: F401
     ShapeOverflow,
     TensorFileError,
     TwoStepOrder,
+    als_iterate,
     choose_order,
     cp_als,
     device_count,
     fit,
     fp64_peak_tflops,
     fp64_peak_tflops_sustained,
+    generate_factors,
     gram_hadamard,
     krp,
     krp_device,
@@ -40,6 +43,7 @@ from .api import (  # noqa: F401
     mttkrp_device,
     mttkrp_one_step,
     mttkrp_two_step,
+    mode_seed,
     solve_psd,
     tensor_norm,
 )

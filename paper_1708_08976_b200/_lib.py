@@ -67,6 +67,8 @@ _SIGS = {
     "dmtk_gpu_solve_psd": (C.c_int, [C.c_int, C.c_int64, dp, C.c_int64, dp, dp]),
     "dmtk_gpu_cp_als": (C.c_int, [T, C.POINTER(AlsConfig), dp, dp, dp, dp, dp, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), dp]),
+    "dmtk_gpu_als_iterate": (C.c_int, [T, C.POINTER(AlsConfig), C.c_int, dpp, i64p, i64p, dp, C.c_int64,
+                                       C.c_double, C.c_int, dp, dp, dp]),
     "dmtk_gpu_fit": (C.c_int, [T, C.c_int, dpp, i64p, i64p, dp, C.c_int64, C.c_int, dp]),
     "dmtk_gpu_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "dmtk_gpu_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),

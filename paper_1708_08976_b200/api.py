@@ -88,6 +88,22 @@ def device_count() -> int:
     return n.value
 
 
+# value distributions of the seeded generator (dmtk_gpu.h DMTK_GPU_DIST_*)
+DISTS = {"uniform": 0, "ones": 1, "signed": 2, "normal": 3, "symslice": 4}
+
+
+def mode_seed(seed: int, mode: int) -> int:
+    """bench.cpp:26-28"""
+    return (seed + 0x9E3779B97F4A7C15 * (mode + 1)) & 0xFFFFFFFFFFFFFFFF
+
+
+def generate_factors(dims: Sequence[int], rank: int, seed: int, dist: str = "uniform", device: int = 0):
+    """dmtk::gen_factors (bench.cpp:108-116) in HBM: factor n is the
+    rows x rank stream of mode_seed(seed, n), transformed like `dist`.
+    Returns one 1-way DenseTensor per factor (row-major values)."""
+    return [DenseTensor.generate((int(d) * rank,), mode_seed(seed, n), dist, device) for n, d in enumerate(dims)]
+
+
 class DenseTensor:
     """Dense FP64 tensor in natural order (tensor.hpp:19-38).
 
@@ -127,14 +143,24 @@ class DenseTensor:
     @classmethod
     def generate(cls, dims: Sequence[int], seed: int, dist: str = "uniform", device: int = 0) -> "DenseTensor":
         """dmtk::gen_tensor (bench.cpp:88-97) generated in HBM: the reference's
-        mt19937_64(seed) uniform(0,1) draws bitwise, or Dist::ones."""
-        if dist not in ("uniform", "ones"):
+        mt19937_64(seed) uniform(0,1) draws bitwise, or Dist::ones; the
+        BASELINE configs' other distributions ("signed" U[-1,1), "normal"
+        N(0,1), "symslice" fMRI slices) as fixed transforms of the same draws
+        (DMTK_GPU_DIST_* in dmtk_gpu.h)."""
+        if dist not in DISTS:
             raise InvalidArgument("gen_tensor: unknown distribution")
         t = cls(dims, None, device)
         d = _i64(t.dims)
         _check(lib.dmtk_gpu_tensor_generate(device, len(d), d.ctypes.data_as(_lib.i64p), C.c_uint64(seed),
-                                            0 if dist == "uniform" else 1, C.byref(t._handle)))
+                                            DISTS[dist], C.byref(t._handle)))
         return t
+
+    def device_ptr(self) -> int:
+        """Device address of the values (natural order, or the padded layout
+        of an odd first extent: row pitch dims[0] + 1)."""
+        p = C.c_void_p()
+        _check(lib.dmtk_gpu_tensor_info(self.handle(), None, None, C.byref(p)))
+        return int(p.value or 0)
 
     def pack_symmetric01(self) -> "DenseTensor":
         """A packed copy of a tensor symmetric in modes 0 and 1 (upper triangle
@@ -442,6 +468,30 @@ def cp_als(x: DenseTensor, config: AlsConfig) -> AlsResult:
              for i in range(k.value)]
     return AlsResult(KruskalModel(factors, lam[:config.rank].copy()),
                      AlsTrace(iters, bool(zero.value), float(norm[0])))
+
+
+def als_iterate(x: DenseTensor, model: KruskalModel, config: AlsConfig, norm_x: float,
+                iter_index: int) -> AlsIterRecord:
+    """dmtk::als_iterate (cp_als.hpp:74-75): one Gauss-Seidel sweep of `model`
+    (updated in place: factors and lambda_) on the device; the fit comes from
+    the last mode's MTTKRP (cp_als.cpp:122-158)."""
+    mats = [np.ascontiguousarray(m, dtype=np.float64) for m in model.factors]
+    ptrs = (_lib.dp * len(mats))(*[_dp(m) for m in mats])
+    rows = _i64([m.shape[0] for m in mats])
+    cols = _i64([m.shape[1] if m.ndim == 2 else 0 for m in mats]) if mats else _i64([0])
+    lam = np.array(model.lambda_, dtype=np.float64, copy=True)
+    cfg = _lib.AlsConfig(config.rank, config.max_iters, config.tol, config.seed, config.threads,
+                         int(config.algo), int(config.order), 0)
+    f4 = np.zeros(4)
+    sec = np.zeros(1)
+    msec = np.zeros(max(len(mats), 1))
+    _check(lib.dmtk_gpu_als_iterate(x.handle(), C.byref(cfg), len(mats), ptrs, rows.ctypes.data_as(_lib.i64p),
+                                    cols.ctypes.data_as(_lib.i64p), _dp(lam), lam.size, float(norm_x),
+                                    int(iter_index), _dp(f4), _dp(sec), _dp(msec)))
+    model.factors = mats
+    model.lambda_ = lam
+    return AlsIterRecord(int(iter_index), FitResult(float(f4[0]), float(f4[1]), float(f4[2]), bool(f4[3])),
+                         list(msec[:len(mats)]), float(sec[0]))
 
 
 def fit(x: DenseTensor, model: KruskalModel, threads: int = 1) -> FitResult:

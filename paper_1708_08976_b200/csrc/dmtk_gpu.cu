@@ -231,6 +231,18 @@ struct dmtk_gpu_tensor_s {
     // tensor maps (they hold the base address) are cached per tensor; plans
     // and CSR slot maps per shape (plans_of / csrs_of)
     std::map<std::array<long long, 7>, CUtensorMap> maps;  // (kind, L, I, R, BK, BI, BJ)
+    dmtk_gpu_tensor_s() = default;
+    dmtk_gpu_tensor_s(const dmtk_gpu_tensor_s&) = delete;
+    dmtk_gpu_tensor_s& operator=(const dmtk_gpu_tensor_s&) = delete;
+    // a handle dropped on an error path (or freed) releases its own device
+    // buffer: the library's allocation, or the padded copy of a borrowed one
+    ~dmtk_gpu_tensor_s() {
+        if ((owned || user) && d) {
+            cudaSetDevice(device);
+            cudaFree(const_cast<double*>(d));  // stream-ordered allocations: implicit sync
+            cudaGetLastError();
+        }
+    }
 };
 
 namespace dmtkg {
@@ -928,7 +940,7 @@ static void tune_store(const TuneKey& k, const TuneChoice& c) {
         }
     }
 }
-static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s) {
+static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s, bool* deferred = nullptr) {
     static const bool off = [] {
         const char* e = std::getenv("DMTK_GPU_AUTOTUNE");
         return e && std::string(e) == "0";
@@ -939,7 +951,12 @@ static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s) {
     }();
     if (off || t.ptotal * 8 < min_bytes) return false;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return false;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) {
+        // only the capture prevents timing: the modelled plan is used for this
+        // call but not cached, so a later uncaptured call still measures
+        if (deferred) *deferred = true;
+        return false;
+    }
     return true;
 }
 
@@ -997,6 +1014,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
     ModePlan pre;  // plan chosen while routing (boundary 1-step / 2-step views)
     bool have_pre = false;
     const double* ones = ctx.ones.p;
+    bool tune_deferred = false;  // measured selection skipped only because the stream is captured
 
     if (algo == DMTK_GPU_BASELINE) {
         // explicit matricization + full KRP + one contraction (mttkrp.cpp:250-304)
@@ -1110,7 +1128,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     // Large tensors: the modelled choice misses DRAM effects (K-major
                     // tiles whose rows lie megabytes apart stream at ~4.5 TB/s), so
                     // the candidates are timed once per shape and the fastest kept
-                    if (force_s == 0 && tune_enabled(t, s)) {
+                    if (force_s == 0 && tune_enabled(t, s, &tune_deferred)) {
                         const TuneKey tk{t.pdims, mode, C, t.d != nullptr && (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
                         TuneChoice tc;
                         if (!tune_lookup(tk, tc)) {
@@ -1161,10 +1179,12 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     }
                 }
                 pre.variant = best_s;
-                auto e = std::make_unique<PlanCacheEntry>();
-                e->mp = pre;
-                e->best_s = best_s;
-                plans[pkey] = std::move(e);
+                if (!tune_deferred) {
+                    auto e = std::make_unique<PlanCacheEntry>();
+                    e->mp = pre;
+                    e->best_s = best_s;
+                    plans[pkey] = std::move(e);
+                }
             }
             gens_for(best_s, bgen, sgen);
         } else {
@@ -1207,7 +1227,7 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                 ModePlan chosen = left ? pl : pr;
                 // large tensors: time the two orders (and the left order with
                 // BJ = 1 row tiles) once per shape, as for the boundary views
-                if (pr.kind != kGeneric && pl.kind != kGeneric && tune_enabled(t, s)) {
+                if (pr.kind != kGeneric && pl.kind != kGeneric && tune_enabled(t, s, &tune_deferred)) {
                     const TuneKey tk{t.pdims, mode, C, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
                     TuneChoice tc;
                     const ModePlan pl1 = plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C, kTcKJ,
@@ -1254,10 +1274,12 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     ord = tc.s;
                     chosen = tc.rb ? order_view(tc) : (ord == DMTK_GPU_ORDER_RIGHT ? pr : (tc.bj1 ? pl1 : pl));
                 }
-                auto e = std::make_unique<PlanCacheEntry>();
-                e->mp = chosen;
-                e->ord = ord;
-                plans[pkey] = std::move(e);
+                if (!tune_deferred) {
+                    auto e = std::make_unique<PlanCacheEntry>();
+                    e->mp = chosen;
+                    e->ord = ord;
+                    plans[pkey] = std::move(e);
+                }
             }
         }
         if (ord == DMTK_GPU_ORDER_RIGHT) {
@@ -1286,9 +1308,12 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
             mp = pit->second->mp;
         } else {
             mp = plan_mode(vdims, vmode, C, kind, ctx.sms);
-            auto e = std::make_unique<PlanCacheEntry>();
-            e->mp = mp;
-            plans[pkey] = std::move(e);
+            if (!tune_deferred) {
+                auto e = std::make_unique<PlanCacheEntry>();
+                e->mp = mp;
+                e->ord = order;
+                plans[pkey] = std::move(e);
+            }
         }
     }
     if (mode == 0) mp.out_rows = std::min(mp.out_rows, t.dims[0]);  // drop a pad row
@@ -1540,7 +1565,10 @@ int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t
     return guarded([&] {
         auto d = checked_dims(ndim, dims);
         if (!out) fail(DMTK_GPU_EINVAL, "gen_tensor: null output");
-        if (dist != 0 && dist != 1) fail(DMTK_GPU_EINVAL, "gen_tensor: unknown distribution");
+        if (dist < DMTK_GPU_DIST_UNIFORM || dist > DMTK_GPU_DIST_SYMSLICE)
+            fail(DMTK_GPU_EINVAL, "gen_tensor: unknown distribution");
+        if (dist == DMTK_GPU_DIST_SYMSLICE && (ndim < 2 || d[0] != d[1]))
+            fail(DMTK_GPU_EINVAL, "gen_tensor: symmetric slices need an order >= 2 tensor with I_0 == I_1");
         Context& ctx = context(device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(device));
@@ -1571,8 +1599,22 @@ int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t
                 uint64_t* scratch = nullptr;
                 CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), dmtkg::mt64_scratch_words(ctx.sms) * 8,
                                    ctx.stream));
-                dmtkg::mt64_generate(p, t->total, d[0], t->pdims[0], seed, ctx.sms, scratch, ctx.stream);
-                CK(cudaGetLastError());
+                if (dist == DMTK_GPU_DIST_UNIFORM) {
+                    dmtkg::mt64_generate(p, t->total, d[0], t->pdims[0], seed, ctx.sms, scratch, ctx.stream);
+                    count_launch();
+                    CK(cudaGetLastError());
+                } else {  // the uniforms into a scratch buffer, then the transform into the layout
+                    const long long nu = gen_dist_uniforms(dist, t->total, d[0]);
+                    double* u = nullptr;
+                    CK(cudaMallocAsync(reinterpret_cast<void**>(&u), static_cast<size_t>(std::max(nu, 1LL)) * 8,
+                                       ctx.stream));
+                    dmtkg::mt64_generate(u, nu, nu, nu, seed, ctx.sms, scratch, ctx.stream);
+                    count_launch();
+                    CK(cudaGetLastError());
+                    launch_gen_dist(u, t->total, dist, d[0], d[0], t->pdims[0], p, ctx.sms, ctx.stream);
+                    check_launch("gen_dist");
+                    CK(cudaFreeAsync(u, ctx.stream));
+                }
                 CK(cudaFreeAsync(scratch, ctx.stream));
             }
         }
@@ -1650,6 +1692,16 @@ int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out) {
         }
         auto d = checked_dims(static_cast<int>(n), dims.data());  // Shape(dims): overflow check
         if (static_cast<int>(n) > kMaxFactors + 1) fail(DMTK_GPU_EINVAL, "dmtk_gpu: tensor order above 13 unsupported");
+        // the reference reads the payload in one piece: same truncation message
+        // (bytes available after the header) before any chunk is read -- and
+        // before the device buffer is allocated
+        struct stat st {};
+        if (fstat(fileno(f), &st) != 0) fail(DMTK_GPU_EIO, std::string("cannot stat '") + path + "'");
+        const uint64_t payload = static_cast<uint64_t>(prod(d, 0, static_cast<int>(n))) * 8;
+        const uint64_t avail = static_cast<uint64_t>(st.st_size) > offset ? static_cast<uint64_t>(st.st_size) - offset : 0;
+        if (avail < payload)
+            fail(DMTK_GPU_EIO, "tensor file truncated reading payload: expected " + std::to_string(payload) +
+                                   " bytes at offset " + std::to_string(offset) + ", got " + std::to_string(avail));
         Context& ctx = context(device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(device));
@@ -1688,15 +1740,6 @@ int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out) {
             }
         } cleanup{stage, done, ctx.stream};
         const size_t pitch = static_cast<size_t>(t->pdims[0]) * sizeof(double);
-        // the reference reads the payload in one piece: same truncation message
-        // (bytes available after the header) before any chunk is read
-        struct stat st {};
-        if (fstat(fileno(f), &st) != 0) fail(DMTK_GPU_EIO, std::string("cannot stat '") + path + "'");
-        const uint64_t payload = static_cast<uint64_t>(t->total) * 8;
-        const uint64_t avail = static_cast<uint64_t>(st.st_size) > offset ? static_cast<uint64_t>(st.st_size) - offset : 0;
-        if (avail < payload)
-            fail(DMTK_GPU_EIO, "tensor file truncated reading payload: expected " + std::to_string(payload) +
-                                   " bytes at offset " + std::to_string(offset) + ", got " + std::to_string(avail));
         // each chunk is read by several threads (parallel page-cache copies)
         const int fd = fileno(f);
         auto pread_all = [&](char* dst, size_t count, uint64_t at) {
@@ -1815,6 +1858,7 @@ int dmtk_gpu_tensor_free(dmtk_gpu_tensor t) {
             cudaSetDevice(t->device);
             cudaFreeAsync(const_cast<double*>(t->d), ctx.stream);
             cudaStreamSynchronize(ctx.stream);
+            t->d = nullptr;
         }
         delete t;
     });
@@ -1888,6 +1932,7 @@ int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factor
                                       " is a boundary mode with a degenerate partial KRP; use one_step instead");
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));  // plans and slot maps are cached per device
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
         ensure_layout(*t, ctx, s);
         std::vector<const double*> f(device_factors, device_factors + N);
@@ -2101,9 +2146,17 @@ static void shard_allreduce(const Shard* sh, double* p, long long n, cudaStream_
     nccl_check(nccl().all_reduce(p, p, static_cast<size_t>(n), ncclFloat64, ncclSum, sh->comm, s), "ncclAllReduce");
 }
 
+// als_iterate (cp_als.hpp:74-75): one sweep from a given model and ||X||
+struct AlsStart {
+    const double* factors;  // concatenated logical factors (row-major)
+    const double* lambda;
+    double norm_x;
+    double* fit4_out;  // fit, rel_residual, abs_residual, defined
+};
+
 static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const Shard* sh, double* factors_out,
                        double* lambda_out, double* fits_out, double* iter_seconds_out, double* mode_seconds_out,
-                       int* n_iters, int* zero_tensor, double* tensor_norm_out) {
+                       int* n_iters, int* zero_tensor, double* tensor_norm_out, const AlsStart* start = nullptr) {
     {
         if (!t) fail(DMTK_GPU_EINVAL, "cp_als: null tensor");
         if (cfg->rank < 1) fail(DMTK_GPU_EINVAL, "cp_als: rank must be >= 1");
@@ -2135,7 +2188,14 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             maxrows = std::max(maxrows, frows[k]);
         }
         std::vector<double> hf(static_cast<size_t>(ptot), 0.0);
-        {
+        if (start) {  // the caller's model (logical rows; pad rows stay zero)
+            long long po = 0, lo = 0;
+            for (int k = 0; k < N; ++k) {
+                std::copy(start->factors + lo, start->factors + lo + t->dims[k] * C, hf.begin() + po);
+                lo += t->dims[k] * C;
+                po += frows[k] * C;
+            }
+        } else {
             long long po = 0;
             for (int k = 0; k < N; ++k) {  // reference stream order; pad rows stay zero
                 // sharded: the stream covers the global last factor, this rank keeps its rows
@@ -2156,7 +2216,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         shb.ensure(static_cast<size_t>(2 * 64 + 8));
         double* sh_sumsq = shb.p;       // C column sums of squares
         double* sh_inner = shb.p + 64;  // the fit's inner product
-        double normx = t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx);
+        double normx = start ? start->norm_x : (t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx));
         if (sh) {  // ||X||^2 summed over the shards
             const double sq = normx * normx;
             CK(cudaMemcpyAsync(sh_inner, &sq, sizeof(double), cudaMemcpyHostToDevice, s));
@@ -2169,7 +2229,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         *tensor_norm_out = normx;
         *n_iters = 0;
         *zero_tensor = 0;
-        if (normx == 0.0) {  // cp_als.cpp:183-189
+        if (normx == 0.0 && !start) {  // cp_als.cpp:183-189 (als_iterate sweeps anyway: fit undefined)
             std::fill(factors_out, factors_out + ftot, 0.0);
             std::fill(lambda_out, lambda_out + C, 0.0);
             *zero_tensor = 1;
@@ -2190,8 +2250,12 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         double* solve_scr = fitb + 4 * fit_slots;
         CK(cudaMemcpyAsync(F.p, hf.data(), hf.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dnorm, &normx, sizeof(double), cudaMemcpyHostToDevice, s));
-        launch_fill(lam, C, 1.0, s);
-        check_launch("fill");
+        if (start) {
+            CK(cudaMemcpyAsync(lam, start->lambda, static_cast<size_t>(C) * sizeof(double), cudaMemcpyHostToDevice, s));
+        } else {
+            launch_fill(lam, C, 1.0, s);
+            check_launch("fill");
+        }
         std::vector<const double*> Uc(N);
         std::vector<double*> Um(N);
         long long off = 0;
@@ -2446,6 +2510,8 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             if (iter_seconds_out) iter_seconds_out[iter - 1] = ms_total * 1e-3;
             fits_out[iter - 1] = f4[4 * iter];
         }
+        if (start && start->fit4_out && done > 0)
+            for (int k = 0; k < 4; ++k) start->fit4_out[k] = f4[4 * done + k];
         for (auto& ge : gexec)
             if (ge) cudaGraphExecDestroy(ge);
         for (auto& e : evs) cudaEventDestroy(e);
@@ -2474,6 +2540,50 @@ int dmtk_gpu_cp_als(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, double* f
     return guarded([&] {
         cp_als_run(t, cfg, nullptr, factors_out, lambda_out, fits_out, iter_seconds_out, mode_seconds_out, n_iters,
                    zero_tensor, tensor_norm_out);
+    });
+}
+
+int dmtk_gpu_als_iterate(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, int nfactors, double* const* factors,
+                         const int64_t* factor_rows, const int64_t* factor_cols, double* lambda, int64_t nlambda,
+                         double norm_x, int iter_index, double* fit4_out, double* seconds_out,
+                         double* mode_seconds_out) {
+    return guarded([&] {
+        if (!t) fail(DMTK_GPU_EINVAL, "als_iterate: null tensor");
+        if (!cfg || !factors || !lambda || !fit4_out) fail(DMTK_GPU_EINVAL, "als_iterate: null argument");
+        if (t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
+        const int N = static_cast<int>(t->dims.size());
+        if (nfactors != N)  // validate_model (cp_als.cpp:74-83)
+            fail(DMTK_GPU_EINVAL, "model has " + std::to_string(nfactors) + " factors for an order-" +
+                                      std::to_string(N) + " tensor");
+        const long long C = nfactors > 0 ? factor_cols[0] : 0;
+        if (nlambda != C) fail(DMTK_GPU_EINVAL, "model lambda length does not match rank");
+        std::vector<const double*> fp(factors, factors + N);
+        validate_factors(t, nfactors, fp.data(), factor_rows, factor_cols, 0, cfg->threads, "mttkrp");
+        (void)iter_index;  // the record's index only (AlsIterRecord::iter)
+        long long tot = 0;
+        for (int k = 0; k < N; ++k) tot += t->dims[k] * C;
+        std::vector<double> cat(static_cast<size_t>(tot));
+        long long off = 0;
+        for (int k = 0; k < N; ++k) {
+            std::copy(factors[k], factors[k] + t->dims[k] * C, cat.begin() + off);
+            off += t->dims[k] * C;
+        }
+        dmtk_gpu_als_config c = *cfg;
+        c.rank = C;
+        c.max_iters = 1;
+        c.tol = 0.0;
+        c.dimtree = 0;
+        const AlsStart st{cat.data(), lambda, norm_x, fit4_out};
+        std::vector<double> out(static_cast<size_t>(tot));
+        double fit = 0, sec = 0, normo = 0;
+        int n_it = 0, zero = 0;
+        cp_als_run(t, &c, nullptr, out.data(), lambda, &fit, &sec, mode_seconds_out, &n_it, &zero, &normo, &st);
+        off = 0;
+        for (int k = 0; k < N; ++k) {
+            std::copy(out.begin() + off, out.begin() + off + t->dims[k] * C, factors[k]);
+            off += t->dims[k] * C;
+        }
+        if (seconds_out) *seconds_out = sec;
     });
 }
 

@@ -57,6 +57,12 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s);
 size_t mt64_scratch_words(int nsm);
 void mt64_generate(double* dst, long long n, long long d0, long long pd0, uint64_t seed, int nsm,
                    uint64_t* dev_scratch, cudaStream_t s);
+// gen_dist.cu: value transforms of the seeded uniforms (dist 2 U[-1,1), 3 N(0,1)
+// Box-Muller, 4 symmetric fMRI slices with tanh(0.3 z) off-diagonals), bitwise
+// equal to the test-side restatement; u holds gen_dist_uniforms(...) draws
+long long gen_dist_uniforms(int dist, long long total, long long I);
+void launch_gen_dist(const double* u, long long total, int dist, long long I, long long d0, long long pd0,
+                     double* dst, int nsm, cudaStream_t s);
 // CP-ALS with cached Grams
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);

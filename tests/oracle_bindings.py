@@ -72,6 +72,14 @@ class Oracle:
         L.orc_normalize_mode.argtypes = [_dp, C.c_int64, C.c_int64, _dp]
         L.orc_fit_from_last_mode.restype = OrcFit
         L.orc_fit_from_last_mode.argtypes = [C.c_double, _dp, C.c_int64, C.c_int64, _dp, _dp, _dp]
+        L.orc_gen_dist.restype = C.c_int
+        L.orc_gen_dist.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip, C.c_int, _dp]
+        L.orc_gen_factors_dist.restype = C.c_int
+        L.orc_gen_factors_dist.argtypes = [C.c_int, _ip, C.c_int64, C.c_uint64, C.c_int, _dp]
+        L.orc_box_muller.restype = C.c_double
+        L.orc_box_muller.argtypes = [C.c_double, C.c_double, C.c_int]
+        L.orc_tanh_portable.restype = C.c_double
+        L.orc_tanh_portable.argtypes = [C.c_double]
         L.orc_cp_als.restype = C.c_int
         L.orc_cp_als.argtypes = [C.c_int, _ip, _dp, C.c_int64, C.c_int, C.c_double, C.c_uint64,
                                  _dp, _dp, _dp, C.POINTER(C.c_int)]
@@ -90,6 +98,23 @@ class Oracle:
         d = _i64(dims)
         out = np.empty(int(d.sum()) * rank, dtype=np.float64)
         self.L.orc_gen_factors(len(d), d.ctypes.data_as(_ip), rank, seed, _d(out))
+        return _split(out, dims, rank)
+
+    DISTS = {"uniform": 0, "ones": 1, "signed": 2, "normal": 3, "symslice": 4}
+
+    def gen_dist(self, dims, seed: int, dist: str = "uniform", threads: int = 0) -> np.ndarray:
+        """gen_tensor with the BASELINE distributions (oracle.c, bitwise the device's)."""
+        d = _i64(dims)
+        out = np.empty(int(np.prod(d)), dtype=np.float64)
+        rc = self.L.orc_gen_dist(seed, self.DISTS[dist], len(d), d.ctypes.data_as(_ip),
+                                 threads or (os.cpu_count() or 1), _d(out))
+        assert rc == 0, "orc_gen_dist rejected its arguments"
+        return out
+
+    def gen_factors_dist(self, dims, rank: int, seed: int, dist: str = "uniform"):
+        d = _i64(dims)
+        out = np.empty(int(d.sum()) * rank, dtype=np.float64)
+        assert self.L.orc_gen_factors_dist(len(d), d.ctypes.data_as(_ip), rank, seed, self.DISTS[dist], _d(out)) == 0
         return _split(out, dims, rank)
 
     def kruskal_random(self, dims, rank: int, seed: int):
@@ -195,6 +220,8 @@ class Ref:
         L.ref_cp_als.argtypes = [C.c_int, _ip, _dp, C.c_int64, C.c_int, C.c_double, C.c_uint64, C.c_int,
                                  C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int), _dp]
+        L.ref_als_iterate.argtypes = [C.c_int, _ip, _dp, C.c_int64, _dp, _dp, C.c_int, C.c_int, C.c_int,
+                                      C.c_double, C.c_int, _dp, _dp]
         L.ref_fit.argtypes = [C.c_int, _ip, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]
         L.ref_write_tensor.argtypes = [C.c_char_p, C.c_int, _ip, _dp]
         L.ref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), _ip, _dp, C.c_int64]
@@ -314,6 +341,20 @@ class Ref:
         k = n.value
         return {"factors": _split(f, dims, rank), "lambda": lam, "fits": fits[:k].copy(),
                 "iter_seconds": secs[:k].copy(), "zero_tensor": bool(zero.value), "norm_x": float(normx[0])}
+
+    def als_iterate(self, x, dims, factors, lam, norm_x: float, iter_index: int = 1, threads: int = 1,
+                    algo: str = "automatic", order: str = "automatic"):
+        """dmtk::als_iterate (cp_als.hpp:74-75): one sweep; returns (factors, lambda, fit4, seconds)."""
+        d = _i64(dims)
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        rank = np.asarray(factors[0]).shape[1]
+        cat = np.ascontiguousarray(np.concatenate([np.asarray(m, dtype=np.float64).reshape(-1) for m in factors]))
+        lam = np.array(lam, dtype=np.float64, copy=True)
+        out = np.zeros(4, dtype=np.float64)
+        sec = np.zeros(1, dtype=np.float64)
+        self._check(self.L.ref_als_iterate(len(d), d.ctypes.data_as(_ip), _d(x), rank, _d(cat), _d(lam), threads,
+                                           self.ALGO[algo], self.ORDER[order], norm_x, iter_index, _d(out), _d(sec)))
+        return _split(cat, dims, rank), lam, out, float(sec[0])
 
     def fit(self, x, dims, factors, lam, threads: int = 1):
         d = _i64(dims)

@@ -40,8 +40,31 @@ def test_generate_ones_and_mttkrp(oracle):
         assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
 
 
+@pytest.mark.parametrize("dist,dims", [("signed", (9, 11, 13)), ("signed", (101, 100, 90)),
+                                       ("normal", (7,)), ("normal", (9, 8, 7)), ("normal", (101, 100, 91)),
+                                       ("normal", (180, 180, 60)),
+                                       ("symslice", (5, 5, 7)), ("symslice", (6, 6, 4, 3)),
+                                       ("symslice", (100, 100, 120, 8)), ("symslice", (33, 33, 5))])
+def test_generate_distributions_bitwise(oracle, dist, dims):
+    """BASELINE configs 3-5's distributions: the device transform of the
+    reference stream equals the host restatement (oracle.c) bit for bit."""
+    t = dg.DenseTensor.generate(dims, 21, dist)
+    assert np.array_equal(t.download(), oracle.gen_dist(dims, 21, dist))
+
+
+def test_generate_factors_distributions(oracle):
+    dims = (180, 64, 7)
+    for dist in ("uniform", "signed", "normal"):
+        dev = dg.generate_factors(dims, 25, 5, dist)
+        want = oracle.gen_factors_dist(dims, 25, 5, dist)
+        for k, t in enumerate(dev):
+            assert np.array_equal(t.download().reshape(dims[k], 25), want[k]), (dist, k)
+
+
 def test_generate_validation():
     with pytest.raises(dg.InvalidArgument):
-        dg.DenseTensor.generate((2, 3), 1, dist="normal")
+        dg.DenseTensor.generate((2, 3), 1, dist="gamma")
+    with pytest.raises(dg.InvalidArgument):
+        dg.DenseTensor.generate((4, 5, 3), 1, dist="symslice")
     with pytest.raises(ValueError):
         dg.DenseTensor.generate((2, 0, 3), 1)
