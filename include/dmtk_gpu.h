@@ -116,6 +116,10 @@ int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out);
  * the reference's CP-ALS on the full tensor -- and dmtk_gpu_tensor_norm (of the
  * full tensor); the other calls reject it. */
 int dmtk_gpu_tensor_pack_sym01(dmtk_gpu_tensor t, dmtk_gpu_tensor* out);
+/* Last-mode slab: a new device tensor holding the rows [lo, hi)
+ * of the slowest mode of t (one contiguous device-to-device copy in the
+ * natural layout), e.g. one rank's shard of a tensor generated whole. */
+int dmtk_gpu_tensor_slab(dmtk_gpu_tensor t, int64_t lo, int64_t hi, dmtk_gpu_tensor* out);
 /* The tensor's values back to host memory in natural order (total doubles). */
 int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out);
 

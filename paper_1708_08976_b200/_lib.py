@@ -53,6 +53,7 @@ _SIGS = {
     "dmtk_gpu_tensor_generate": (C.c_int, [C.c_int, C.c_int, i64p, C.c_uint64, C.c_int, C.POINTER(T)]),
     "dmtk_gpu_mt64_jump": (C.c_int, [C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]),
     "dmtk_gpu_tensor_download": (C.c_int, [T, dp]),
+    "dmtk_gpu_tensor_slab": (C.c_int, [T, C.c_int64, C.c_int64, C.POINTER(T)]),
     "dmtk_gpu_tensor_pack_sym01": (C.c_int, [T, C.POINTER(T)]),
     "dmtk_gpu_mttkrp": (C.c_int, [T, C.c_int, dpp, i64p, i64p, C.c_int64, C.c_int, C.c_int, C.c_int, dp,
                                   C.POINTER(Times)]),

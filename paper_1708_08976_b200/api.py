@@ -173,6 +173,15 @@ class DenseTensor:
         t._owner = self  # the packed copy is independent; keep the source alive anyway
         return t
 
+    def slab(self, lo: int, hi: int) -> "DenseTensor":
+        """The last-mode rows [lo, hi) as a new device tensor (a rank's shard,
+        SURVEY 8e; dmtk_gpu_tensor_slab)."""
+        h = C.c_void_p()
+        _check(lib.dmtk_gpu_tensor_slab(self.handle(), int(lo), int(hi), C.byref(h)))
+        t = DenseTensor(self.dims[:-1] + (int(hi) - int(lo),), None, self.device)
+        t._handle = h
+        return t
+
     def download(self) -> np.ndarray:
         """The values in natural order, from the device copy."""
         out = np.empty(self.total)

@@ -1831,6 +1831,44 @@ int dmtk_gpu_tensor_pack_sym01(dmtk_gpu_tensor t, dmtk_gpu_tensor* out) {
     });
 }
 
+int dmtk_gpu_tensor_slab(dmtk_gpu_tensor t, int64_t lo, int64_t hi, dmtk_gpu_tensor* out) {
+    return guarded([&] {
+        if (!t || !out) fail(DMTK_GPU_EINVAL, "tensor_slab: null argument");
+        if (t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
+        const int N = static_cast<int>(t->dims.size());
+        if (lo < 0 || hi <= lo || hi > t->dims[N - 1])
+            fail(DMTK_GPU_ERANGE, "tensor_slab: last-mode rows [" + std::to_string(lo) + ", " + std::to_string(hi) +
+                                      ") outside [0, " + std::to_string(t->dims[N - 1]) + ")");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));
+        auto p = std::make_unique<dmtk_gpu_tensor_s>();
+        p->device = t->device;
+        p->dims = t->dims;
+        p->dims[N - 1] = hi - lo;
+        p->total = prod(p->dims, 0, N);
+        p->pdims = t->pdims;
+        long long plane = prod(t->pdims, 0, N - 1), first = lo * plane, count = (hi - lo) * plane;
+        if (N == 1) {  // a 1-way slab: same layout rule as an upload (even physical extent)
+            p->pdims[0] = (hi - lo) + ((hi - lo) & 1);
+            plane = 1;
+            first = lo;
+            count = hi - lo;
+        }
+        p->ptotal = prod(p->pdims, 0, N);
+        double* buf = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), static_cast<size_t>(p->ptotal) * sizeof(double), ctx.stream));
+        p->d = buf;
+        p->owned = true;
+        CK(cudaMemcpyAsync(buf, t->d + first, static_cast<size_t>(count) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx.stream));
+        if (p->ptotal > count)
+            CK(cudaMemsetAsync(buf + count, 0, static_cast<size_t>(p->ptotal - count) * sizeof(double), ctx.stream));
+        CK(cudaStreamSynchronize(ctx.stream));
+        *out = p.release();
+    });
+}
+
 int dmtk_gpu_tensor_download(dmtk_gpu_tensor t, double* host_out) {
     return guarded([&] {
         if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
