@@ -238,6 +238,14 @@ typedef struct dmtk_gpu_comm_s* dmtk_gpu_comm;
 int dmtk_gpu_comm_unique_id(unsigned char* id128);
 int dmtk_gpu_comm_init(const unsigned char* id128, int rank, int world, int device, dmtk_gpu_comm* out);
 int dmtk_gpu_comm_free(dmtk_gpu_comm comm);
+/* Loopback communicators (tests of the sharded path without a second GPU):
+ * `world` (1..16) virtual ranks on one device, comms_out[k] = rank k. Each
+ * rank's dmtk_gpu_cp_als_sharded must run concurrently in its own host thread
+ * (the all-reduces are host barriers plus stream events; ranks get separate
+ * contexts and streams). Same exchanges, same code path as the NCCL
+ * communicator except that the sweeps run eagerly (no CUDA graphs). Free
+ * every handle with dmtk_gpu_comm_free. */
+int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out);
 int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t last_extent, int64_t last_lo,
                             const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out, double* fits_out,
                             double* iter_seconds_out, double* mode_seconds_out, int* n_iters, int* zero_tensor,

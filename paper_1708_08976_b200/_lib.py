@@ -74,6 +74,7 @@ _SIGS = {
     "dmtk_gpu_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "dmtk_gpu_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dmtk_gpu_comm_free": (C.c_int, [C.c_void_p]),
+    "dmtk_gpu_comm_loopback": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dmtk_gpu_cp_als_sharded": (C.c_int, [T, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(AlsConfig), dp, dp, dp, dp,
                                           dp, C.POINTER(C.c_int), C.POINTER(C.c_int), dp]),
     "dmtk_gpu_fp64_peak": (C.c_int, [C.c_int, dp]),

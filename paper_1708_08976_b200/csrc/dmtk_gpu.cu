@@ -11,6 +11,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -142,13 +143,19 @@ struct Context {
 };
 
 static std::mutex g_ctx_mu;
-static std::map<int, std::unique_ptr<Context>> g_ctx;
+static std::map<std::pair<int, int>, std::unique_ptr<Context>> g_ctx;
+
+// Execution slot of the calling thread: 0 for every public call, k + 1 while
+// a thread runs loopback rank k of a sharded CP-ALS (dmtk_gpu_comm_loopback):
+// each virtual rank gets its own context (stream, workspaces, mutex) and its
+// own plan / slot-map caches, so P ranks can run concurrently on one device.
+static thread_local int g_slot = 0;
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 static Context& context(int device) {
     std::lock_guard<std::mutex> lk(g_ctx_mu);
-    auto it = g_ctx.find(device);
+    auto it = g_ctx.find({device, g_slot});
     if (it != g_ctx.end()) return *it->second;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -186,7 +193,7 @@ static Context& context(int device) {
     }
     CK(cudaStreamSynchronize(c->stream));
     Context& ref = *c;
-    g_ctx[device] = std::move(c);
+    g_ctx[{device, g_slot}] = std::move(c);
     return ref;
 }
 
@@ -614,16 +621,17 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
 // are never dropped (CUDA graphs captured by CP-ALS hold the slot-map
 // pointers); callers hold the device context's mutex.
 struct ShapeKey {
-    int device;
+    int device, slot;
     std::vector<long long> dims, pdims;
     bool sym01, aligned;
     bool operator<(const ShapeKey& o) const {
-        return std::tie(device, dims, pdims, sym01, aligned) < std::tie(o.device, o.dims, o.pdims, o.sym01, o.aligned);
+        return std::tie(device, slot, dims, pdims, sym01, aligned) <
+               std::tie(o.device, o.slot, o.dims, o.pdims, o.sym01, o.aligned);
     }
 };
 
 static ShapeKey shape_key(const dmtk_gpu_tensor_s& t) {
-    return ShapeKey{t.device, t.dims, t.pdims, t.sym01, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
+    return ShapeKey{t.device, g_slot, t.dims, t.pdims, t.sym01, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
 }
 
 static std::map<long long, std::unique_ptr<PlanCacheEntry>>& plans_of(const dmtk_gpu_tensor_s& t) {
@@ -2173,15 +2181,69 @@ static void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) fail(DMTK_GPU_ERUNTIME, std::string(what) + ": " + nccl().error_string(r));
 }
 
+// Loopback group (dmtk_gpu_comm_loopback): P virtual ranks of one process on
+// one device, each driven by its own host thread with its own stream. An
+// all-reduce publishes every rank's buffer at a host barrier, then each rank
+// sums all P buffers in rank order into its own scratch on its stream (after
+// stream-waiting on the other ranks' "ready" events), and copies the sum back
+// once every rank has finished reading (second barrier + "done" events). No
+// kernel ever waits on another kernel: ranks are ordered only by stream
+// events, so they cannot deadlock however the device schedules them. The
+// production NCCL path is unchanged; the loopback runs the same sharded CP-ALS
+// code (eagerly: no CUDA graphs, whose replays would race the host barrier).
+struct LoopGroup {
+    int P = 0, device = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long generation = 0;
+    std::vector<double*> bufs;
+    std::vector<cudaEvent_t> ready, done;
+    std::vector<DevBuf> sums;
+    int refs = 0;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long gen = generation;
+        if (++arrived == P) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct Shard {
-    ncclComm_t comm;
+    ncclComm_t comm;        // NCCL communicator, or
+    LoopGroup* loop;        // the loopback group (then comm is unused)
+    int rank;               // this rank in the group
     long long last_extent;  // global extent of the last mode
     long long last_lo;      // this rank's first last-mode row
 };
 
 static void shard_allreduce(const Shard* sh, double* p, long long n, cudaStream_t s) {
     if (!sh || n <= 0) return;
-    nccl_check(nccl().all_reduce(p, p, static_cast<size_t>(n), ncclFloat64, ncclSum, sh->comm, s), "ncclAllReduce");
+    if (!sh->loop) {
+        nccl_check(nccl().all_reduce(p, p, static_cast<size_t>(n), ncclFloat64, ncclSum, sh->comm, s),
+                   "ncclAllReduce");
+        return;
+    }
+    LoopGroup& g = *sh->loop;
+    const int r = sh->rank;
+    CK(cudaEventRecord(g.ready[r], s));
+    g.bufs[r] = p;
+    g.barrier();  // every rank's buffer and ready event are published
+    for (int k = 0; k < g.P; ++k)
+        if (k != r) CK(cudaStreamWaitEvent(s, g.ready[k], 0));
+    g.sums[r].ensure(static_cast<size_t>(n));
+    launch_loop_sum(g.bufs.data(), g.P, n, g.sums[r].p, s);
+    check_launch("loop_sum");
+    CK(cudaEventRecord(g.done[r], s));
+    g.barrier();  // every rank has enqueued its reads of the P buffers
+    for (int k = 0; k < g.P; ++k)
+        if (k != r) CK(cudaStreamWaitEvent(s, g.done[k], 0));
+    CK(cudaMemcpyAsync(p, g.sums[r].p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
 // als_iterate (cp_als.hpp:74-75): one sweep from a given model and ||X||
@@ -2494,7 +2556,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
                 if (st == NS - 2) CK(cudaEventRecord(ev[NS - 1], s));
             }
             CK(cudaMemcpyAsync(fitb + 4 * iter, fitb, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-            if (iter == 1 && iters > 1) {  // capture after the eager warm-up iteration
+            if (iter == 1 && iters > 1 && !(sh && sh->loop)) {  // capture after the eager warm-up iteration
                 bool ok = true;
                 for (int st = 0; st < NS && ok; ++st) {
                     cudaGraph_t g = nullptr;
@@ -2627,8 +2689,39 @@ int dmtk_gpu_als_iterate(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, int 
 
 struct dmtk_gpu_comm_s {
     ncclComm_t comm = nullptr;
+    LoopGroup* loop = nullptr;
     int rank = 0, world = 1, device = 0;
 };
+
+int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out) {
+    return guarded([&] {
+        if (!comms_out) fail(DMTK_GPU_EINVAL, "comm_loopback: null argument");
+        if (world < 1 || world > kLoopMax)
+            fail(DMTK_GPU_EINVAL, "comm_loopback: world must be in [1, " + std::to_string(kLoopMax) + "]");
+        context(device);  // validates the device
+        CK(cudaSetDevice(device));
+        auto g = new LoopGroup;
+        g->P = world;
+        g->device = device;
+        g->bufs.assign(world, nullptr);
+        g->ready.resize(world);
+        g->done.resize(world);
+        g->sums.resize(world);
+        for (int k = 0; k < world; ++k) {
+            CK(cudaEventCreateWithFlags(&g->ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&g->done[k], cudaEventDisableTiming));
+        }
+        g->refs = world;
+        for (int k = 0; k < world; ++k) {
+            auto c = new dmtk_gpu_comm_s;
+            c->loop = g;
+            c->rank = k;
+            c->world = world;
+            c->device = device;
+            comms_out[k] = c;
+        }
+    });
+}
 
 int dmtk_gpu_comm_unique_id(unsigned char* id128) {
     return guarded([&] {
@@ -2660,6 +2753,21 @@ int dmtk_gpu_comm_free(dmtk_gpu_comm c) {
     return guarded([&] {
         if (!c) return;
         if (c->comm) nccl().comm_destroy(c->comm);
+        if (c->loop) {
+            LoopGroup* g = c->loop;
+            bool last;
+            {
+                std::lock_guard<std::mutex> lk(g->mu);
+                last = --g->refs == 0;
+            }
+            if (last) {
+                cudaSetDevice(g->device);
+                cudaDeviceSynchronize();
+                for (auto e : g->ready) cudaEventDestroy(e);
+                for (auto e : g->done) cudaEventDestroy(e);
+                delete g;
+            }
+        }
         delete c;
     });
 }
@@ -2672,7 +2780,13 @@ int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t la
         if (!comm) fail(DMTK_GPU_EINVAL, "cp_als_sharded: null communicator");
         if (slab && slab->device != comm->device)
             fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab and the communicator are on different devices");
-        const Shard sh{comm->comm, last_extent, last_lo};
+        const Shard sh{comm->comm, comm->loop, comm->rank, last_extent, last_lo};
+        // a loopback rank runs in its own execution slot (context and caches)
+        struct SlotGuard {
+            int prev;
+            ~SlotGuard() { g_slot = prev; }
+        } guard{g_slot};
+        if (comm->loop) g_slot = 1 + comm->rank;
         cp_als_run(slab, cfg, &sh, factors_out, lambda_out, fits_out, iter_seconds_out, mode_seconds_out, n_iters,
                    zero_tensor, tensor_norm_out);
     });

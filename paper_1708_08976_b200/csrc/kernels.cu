@@ -1196,8 +1196,9 @@ void launch_solve_psd_inverse(const double* H, int n, const double* M, long long
     double* gain = V + 64 * 64;
     const int sm2 = 2 * n * n * 8;
     static std::atomic<unsigned long long> opted{0};
-    if (first_on_device(opted))
+    once_on_device(opted, [] {
         cudaFuncSetAttribute(cholesky_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
+    });
     if (n <= 32)
         cholesky_inverse_rl_kernel<<<1, 32, 0, s>>>(H, n, Hinv, flag);
     else
@@ -1266,4 +1267,28 @@ void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s) {
     dmma_peak_kernel<<<blocks, 256, 0, s>>>(out, iters);
 }
 
+}  // namespace dmtkg
+
+// ---------------------------------------------------------------- loopback
+namespace dmtkg {
+namespace {
+struct LoopPtrs {
+    const double* p[kLoopMax];
+};
+__global__ void loop_sum_kernel(LoopPtrs b, int P, long long n, double* __restrict__ out) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double acc = b.p[0][i];
+        for (int k = 1; k < P; ++k) acc += b.p[k][i];
+        out[i] = acc;
+    }
+}
+}  // namespace
+
+void launch_loop_sum(double* const* bufs, int P, long long n, double* out, cudaStream_t s) {
+    LoopPtrs b{};
+    for (int k = 0; k < P; ++k) b.p[k] = bufs[k];
+    const long long blocks = (n + 255) / 256;
+    loop_sum_kernel<<<static_cast<int>(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(b, P, n, out);
+}
 }  // namespace dmtkg

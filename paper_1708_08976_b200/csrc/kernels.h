@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "mttkrp_plan.h"
 
@@ -11,12 +12,24 @@ namespace dmtkg {
 
 // Function attributes (the shared-memory opt-in) belong to the current
 // device's context: raise them once per device, outside any graph capture.
-inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+// Runs f() (e.g. cudaFuncSetAttribute) once per device before any caller
+// proceeds: concurrent first callers (loopback ranks) wait for it.
+template <class F>
+inline void once_on_device(std::atomic<unsigned long long>& mask, F&& f) {
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
-    return (mask.fetch_or(bit) & bit) == 0;
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    f();
+    mask.fetch_or(bit, std::memory_order_release);
 }
+
+// loopback all-reduce: out = sum of bufs[0..P-1] in rank order (P <= kLoopMax)
+constexpr int kLoopMax = 16;
+void launch_loop_sum(double* const* bufs, int P, long long n, double* out, cudaStream_t s);
 
 void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
                       cudaStream_t s);

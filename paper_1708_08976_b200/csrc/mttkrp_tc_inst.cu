@@ -25,7 +25,7 @@ static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaSt
     if constexpr (tc_has_tail(TAIL)) {
         auto k = mttkrp_tc_kernel<TC_NB, TAIL, KM, TC_RB, EPI>;
         static std::atomic<unsigned long long> opted{0};  // per device; not a stream op (graph-safe)
-        if (first_on_device(opted)) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        once_on_device(opted, [k] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
         k<<<grid, tc_threads(TC_RB), p.smem, s>>>(map, p);
     }
 }
