@@ -11,11 +11,14 @@
 //
 // Device residency: DenseTensor is immutable (tensor.hpp:11-18), so the shim
 // uploads each host tensor once and caches the device copy keyed by
-// (data pointer, shape). Call dmtk::gpu::forget(tensor) before freeing or
-// reusing a buffer that was passed in.
+// (data pointer, shape), validated per call by a sampled fingerprint (a new
+// tensor in a reused buffer is re-uploaded), at most four tensors / 64 GB
+// (LRU). dmtk::gpu::forget(tensor) drops a cached copy early.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -43,22 +46,53 @@ inline void check(int rc) {
 }
 
 namespace detail {
+// Host tensors are uploaded once and kept on the device (DenseTensor is
+// immutable, tensor.hpp:11-18). A cached copy is keyed by (data pointer,
+// shape) and validated by a sampled fingerprint on every call, so a new tensor
+// that reuses a freed buffer's address is uploaded afresh; the cache holds at
+// most kMaxTensors tensors / kMaxBytes (least recently used evicted).
 struct Key {
     const double* p;
     std::vector<std::int64_t> dims;
     bool operator<(const Key& o) const { return std::tie(p, dims) < std::tie(o.p, o.dims); }
 };
+struct Entry {
+    dmtk_gpu_tensor h = nullptr;
+    std::uint64_t fingerprint = 0, bytes = 0, used = 0;
+};
+constexpr std::size_t kMaxTensors = 4;
+constexpr std::uint64_t kMaxBytes = 64ull << 30;
 inline std::mutex& mu() {
     static std::mutex m;
     return m;
 }
-inline std::map<Key, dmtk_gpu_tensor>& registry() {
-    static std::map<Key, dmtk_gpu_tensor> r;
+inline std::map<Key, Entry>& registry() {
+    static std::map<Key, Entry> r;
     return r;
+}
+inline std::uint64_t& clock() {
+    static std::uint64_t c = 0;
+    return c;
 }
 inline int& device() {
     static int d = 0;
     return d;
+}
+// FNV-1a over the bit patterns of the first and last 64 values and 1024
+// evenly spaced ones (about 1 µs-scale host work per call)
+inline std::uint64_t fingerprint(const double* p, std::int64_t n) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&](std::int64_t i) {
+        std::uint64_t b;
+        std::memcpy(&b, p + i, 8);
+        h = (h ^ b) * 1099511628211ull;
+        h = (h ^ static_cast<std::uint64_t>(i)) * 1099511628211ull;
+    };
+    for (std::int64_t i = 0; i < std::min<std::int64_t>(n, 64); ++i) mix(i);
+    for (std::int64_t i = std::max<std::int64_t>(64, n - 64); i < n; ++i) mix(i);
+    if (n > 128)
+        for (std::int64_t k = 0; k < 1024; ++k) mix(64 + (n - 128) * k / 1024);
+    return h;
 }
 }  // namespace detail
 
@@ -67,12 +101,34 @@ inline void set_device(int d) { detail::device() = d; }
 inline dmtk_gpu_tensor handle(const DenseTensor& x) {
     const auto dims = x.shape().dims();
     detail::Key k{x.data(), std::vector<std::int64_t>(dims.begin(), dims.end())};
+    const std::uint64_t fp = detail::fingerprint(x.data(), x.total());
     std::lock_guard<std::mutex> lk(detail::mu());
-    auto it = detail::registry().find(k);
-    if (it != detail::registry().end()) return it->second;
+    auto& reg = detail::registry();
+    auto it = reg.find(k);
+    if (it != reg.end()) {
+        if (it->second.fingerprint == fp) {
+            it->second.used = ++detail::clock();
+            return it->second.h;
+        }
+        dmtk_gpu_tensor_free(it->second.h);  // same address, different tensor
+        reg.erase(it);
+    }
+    const std::uint64_t bytes = static_cast<std::uint64_t>(x.total()) * 8;
+    auto total = [&] {
+        std::uint64_t b = 0;
+        for (auto& e : reg) b += e.second.bytes;
+        return b;
+    };
+    while (!reg.empty() && (reg.size() >= detail::kMaxTensors || total() + bytes > detail::kMaxBytes)) {
+        auto lru = reg.begin();
+        for (auto e = reg.begin(); e != reg.end(); ++e)
+            if (e->second.used < lru->second.used) lru = e;
+        dmtk_gpu_tensor_free(lru->second.h);
+        reg.erase(lru);
+    }
     dmtk_gpu_tensor h = nullptr;
     check(dmtk_gpu_tensor_upload(detail::device(), static_cast<int>(k.dims.size()), k.dims.data(), x.data(), &h));
-    detail::registry()[k] = h;
+    reg[k] = detail::Entry{h, fp, bytes, ++detail::clock()};
     return h;
 }
 
@@ -82,7 +138,7 @@ inline void forget(const DenseTensor& x) {
     std::lock_guard<std::mutex> lk(detail::mu());
     auto it = detail::registry().find(k);
     if (it != detail::registry().end()) {
-        dmtk_gpu_tensor_free(it->second);
+        dmtk_gpu_tensor_free(it->second.h);
         detail::registry().erase(it);
     }
 }
