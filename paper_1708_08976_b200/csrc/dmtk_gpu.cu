@@ -834,16 +834,19 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
 }
 
-// Borrowed tensors keep the caller's layout, but an odd first extent would
-// leave TMA unusable (8-byte cp.async producer, 0.03-0.3 of roofline): repack
-// once into the padded layout of dmtk_gpu_tensor_upload (one pitched D2D
+// Borrowed tensors keep the caller's layout, but an odd first extent or a
+// base that is not 16-byte aligned would leave TMA unusable (8-byte cp.async
+// producer, 0.03-0.3 of roofline): repack once into the (padded) layout of
+// dmtk_gpu_tensor_upload in a library-owned buffer (one pitched D2D
 // copy; the borrowed buffer must stay unchanged while wrapped, as the
 // reference's DenseTensor::borrow requires). Falls back to the cp.async
 // producer when the copy cannot be allocated.
 static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
-    if (t.owned || t.user || t.repack_failed || t.dims[0] % 2 == 0 || t.total == 0) return;
+    const bool odd = t.dims[0] % 2 != 0;
+    const bool unaligned = (reinterpret_cast<uintptr_t>(t.d) & 15) != 0;  // TMA needs a 16-byte base
+    if (t.owned || t.user || t.repack_failed || (!odd && !unaligned) || t.total == 0) return;
     std::vector<long long> pd = t.dims;
-    pd[0] += 1;
+    if (odd) pd[0] += 1;
     const long long pt = prod(pd, 0, static_cast<int>(pd.size()));
     double* p = nullptr;
     if (cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(pt) * sizeof(double), ctx.stream) !=
@@ -857,7 +860,7 @@ static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));  // the borrowed data is final at this call
     CK(cudaMemcpy2DAsync(p, pitch, t.d, static_cast<size_t>(t.dims[0]) * sizeof(double),
                          static_cast<size_t>(t.dims[0]) * sizeof(double), rows, cudaMemcpyDeviceToDevice, ctx.stream));
-    CK(cudaMemset2DAsync(p + t.dims[0], pitch, 0, sizeof(double), rows, ctx.stream));
+    if (odd) CK(cudaMemset2DAsync(p + t.dims[0], pitch, 0, sizeof(double), rows, ctx.stream));
     CK(cudaStreamSynchronize(ctx.stream));
     t.user = t.d;
     t.d = p;
