@@ -2099,7 +2099,7 @@ int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t ra
                            int64_t skip, double* h_out) {
     return guarded([&] {
         if (ndim < 1) fail(DMTK_GPU_EINVAL, "gram_hadamard: no factors");
-        if (rank < 1 || rank > 64) fail(DMTK_GPU_EINVAL, "gram_hadamard: rank must be in [1, 64] on the GPU path");
+        if (rank < 1) fail(DMTK_GPU_EINVAL, "gram_hadamard: rank must be >= 1");
         Context& ctx = context(device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(device));
@@ -2115,8 +2115,19 @@ int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t ra
             dp[k] = ctx.fac.p + off;
             off += rows[k] * rank;
         }
-        ctx.als_small.ensure(64 * 64);
-        gram_hadamard_dev(ctx, r, dp, static_cast<int>(rank), static_cast<int>(skip), ctx.als_small.p, ctx.stream);
+        if (rank > 64) {  // every Gram, then their Hadamard product (als_wide.cu)
+            ctx.als_small.ensure(static_cast<size_t>((ndim + 1) * rank * rank));
+            double* grams = ctx.als_small.p + rank * rank;
+            for (int k = 0; k < ndim; ++k)
+                launch_wide_gram(dp[k], r[k], static_cast<int>(rank), grams + k * rank * rank, ctx.stream);
+            launch_wide_hadamard(grams, ndim, static_cast<int>(rank), static_cast<int>(skip), ctx.als_small.p,
+                                 ctx.stream);
+            count_launch(ndim + 1);
+            ck(cudaGetLastError(), "gram_hadamard");
+        } else {
+            ctx.als_small.ensure(64 * 64);
+            gram_hadamard_dev(ctx, r, dp, static_cast<int>(rank), static_cast<int>(skip), ctx.als_small.p, ctx.stream);
+        }
         CK(cudaMemcpyAsync(h_out, ctx.als_small.p, static_cast<size_t>(rank * rank) * sizeof(double),
                            cudaMemcpyDeviceToHost, ctx.stream));
         CK(cudaStreamSynchronize(ctx.stream));
@@ -2125,19 +2136,24 @@ int dmtk_gpu_gram_hadamard(int device, int ndim, const int64_t* rows, int64_t ra
 
 int dmtk_gpu_solve_psd(int device, int64_t rank, const double* h, int64_t rows, const double* m, double* u_out) {
     return guarded([&] {
-        if (rank < 1 || rank > 64) fail(DMTK_GPU_EINVAL, "solve_psd: rank must be in [1, 64] on the GPU path");
+        if (rank < 1) fail(DMTK_GPU_EINVAL, "solve_psd: rank must be >= 1");
         Context& ctx = context(device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(device));
-        ctx.als_small.ensure(64 * 64 * 4);
-        ctx.scratch.ensure(static_cast<size_t>(2 * rows * rank + 3 * 64 * 64));
+        const long long CM = std::max<long long>(rank, 64);
+        ctx.als_small.ensure(static_cast<size_t>(CM * CM * 4));
+        const long long sd = rank > 64 ? wide_scratch_doubles(static_cast<int>(rank), rows) : 3 * 64 * 64;
+        ctx.scratch.ensure(static_cast<size_t>(2 * rows * rank + sd));
         double* H = ctx.als_small.p;
         double* M = ctx.scratch.p;
         double* U = M + rows * rank;
         double* S = U + rows * rank;
         CK(cudaMemcpyAsync(H, h, static_cast<size_t>(rank * rank) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
         CK(cudaMemcpyAsync(M, m, static_cast<size_t>(rows * rank) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
-        launch_solve_psd(H, static_cast<int>(rank), M, rows, U, S, ctx.flag, ctx.stream);
+        if (rank > 64)
+            launch_wide_solve(H, static_cast<int>(rank), M, rows, U, S, ctx.flag, ctx.stream);
+        else
+            launch_solve_psd(H, static_cast<int>(rank), M, rows, U, S, ctx.flag, ctx.stream);
         count_launch(4);
         ck(cudaGetLastError(), "solve_psd");
         CK(cudaMemcpyAsync(u_out, U, static_cast<size_t>(rows * rank) * sizeof(double), cudaMemcpyDeviceToHost,
@@ -2265,8 +2281,13 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         if (cfg->rank < 1) fail(DMTK_GPU_EINVAL, "cp_als: rank must be >= 1");
         if (cfg->max_iters < 0) fail(DMTK_GPU_EINVAL, "cp_als: max_iters must be >= 0");
         if (cfg->threads < 1) fail(DMTK_GPU_EINVAL, "cp_als: threads must be >= 1");
-        if (cfg->rank > 64) fail(DMTK_GPU_EINVAL, "cp_als: rank above 64 is not supported on the GPU path");
         const int N = static_cast<int>(t->dims.size());
+        // ranks above 64 (the reference takes any rank) run the per-mode sweep
+        // with the global-memory factor update (als_wide.cu); the dimension-tree
+        // and packed sweeps keep their rank <= 64 multi-TTV kernels
+        if (cfg->rank > 64 && (t->sym01 || (cfg->dimtree != 0 && N >= 3)))
+            fail(DMTK_GPU_EINVAL, "cp_als: the dimension-tree and symmetric-packed sweeps need rank <= 64 "
+                                  "(the per-mode sweep takes any rank)");
         if (cfg->algo == DMTK_GPU_TWO_STEP)  // the first (boundary) mode refuses two_step
             fail(DMTK_GPU_EINVAL,
                  "mttkrp_two_step: mode 0 is a boundary mode with a degenerate partial KRP; use one_step instead");
@@ -2315,10 +2336,12 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         }
 
         // (sharded: scalars and small exchange buffers)
+        const bool wide = C > 64;     // global-memory factor update (als_wide.cu)
+        const int CM = std::max(C, 64);
         DevBuf shb;
-        shb.ensure(static_cast<size_t>(2 * 64 + 8));
+        shb.ensure(static_cast<size_t>(2 * CM + 8));
         double* sh_sumsq = shb.p;       // C column sums of squares
-        double* sh_inner = shb.p + 64;  // the fit's inner product
+        double* sh_inner = shb.p + CM;  // the fit's inner product
         double normx = start ? start->norm_x : (t->sym01 ? t->full_norm : tensor_norm_dev(*t, ctx));
         if (sh) {  // ||X||^2 summed over the shards
             const double sq = normx * normx;
@@ -2344,10 +2367,11 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         M.ensure(static_cast<size_t>(maxrows * C));
         const int iters = cfg->max_iters;
         const int fit_slots = std::max(iters, 1) + 1;
-        aux.ensure(static_cast<size_t>(64 + 64 * 64 + N * C * C + 1 + 4 * fit_slots + 3 * 64 * 64 + 64));
+        const long long solve_doubles = wide ? wide_scratch_doubles(C, maxrows) + CM : 3 * 64 * 64 + 64;
+        aux.ensure(static_cast<size_t>(CM + CM * CM + N * C * C + 1 + 4 * fit_slots + solve_doubles));
         double* lam = aux.p;
-        double* H = lam + 64;
-        double* grams = H + 64 * 64;
+        double* H = lam + CM;
+        double* grams = H + CM * CM;
         double* dnorm = grams + N * C * C;
         double* fitb = dnorm + 1;           // slot 0: the graph's fit output; 1..iters: history
         double* solve_scr = fitb + 4 * fit_slots;
@@ -2366,7 +2390,10 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             Um[k] = F.p + off;
             Uc[k] = Um[k];
             off += frows[k] * C;
-            launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
+            if (wide)
+                launch_wide_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);
+            else
+                launch_gram(Um[k], t->dims[k], C, grams + static_cast<long long>(k) * C * C, s);  // cached Grams
             check_launch("gram");
         }
         shard_allreduce(sh, grams + static_cast<long long>(N - 1) * C * C, static_cast<long long>(C) * C, s);
@@ -2374,9 +2401,16 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         // Gram-Hadamard from the cached Grams, solve, normalise, refresh this
         // mode's Gram. The fit reads the last mode's M (cp_als.cpp:149-155).
         const double* fitM = M.p;
+        // (wide: the column sums of squares sit after the solve scratch)
+        double* wide_sumsq = solve_scr + (wide ? wide_scratch_doubles(C, maxrows) : 0);
+        auto update = [&](int n, const double* Mn, double* Gn, bool solve_only) {
+            return wide ? launch_wide_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam, Gn, solve_scr,
+                                                 wide_sumsq, ctx.flag, s, solve_only)
+                        : launch_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam, Gn, solve_scr, ctx.flag,
+                                            s, solve_only);
+        };
         auto als_upd = [&](int n, const double* Mn) {
-            const int nl = launch_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam,
-                                             grams + static_cast<long long>(n) * C * C, solve_scr, ctx.flag, s);
+            const int nl = update(n, Mn, grams + static_cast<long long>(n) * C * C, false);
             count_launch(nl - 1);
             check_launch("als_update");
             if (n == N - 1) fitM = Mn;
@@ -2385,14 +2419,20 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         // Gram are sums over the shards (C and C x C all-reduces).
         auto als_upd_sharded_last = [&](int n, const double* Mn) {
             double* Gn = grams + static_cast<long long>(n) * C * C;
-            const int nl = launch_als_update(grams, N, C, n, H, Mn, t->dims[n], Um[n], lam, Gn, solve_scr, ctx.flag, s,
-                                             /*solve_only*/ true);
+            const int nl = update(n, Mn, Gn, /*solve_only*/ true);
             count_launch(nl - 1);
             check_launch("als_update");
-            launch_col_sumsq(Um[n], t->dims[n], C, sh_sumsq, s);
-            shard_allreduce(sh, sh_sumsq, C, s);
-            launch_normalize_cols_by(Um[n], t->dims[n], C, sh_sumsq, lam, s);
-            launch_gram(Um[n], t->dims[n], C, Gn, s);
+            if (wide) {
+                launch_wide_col_sumsq(Um[n], t->dims[n], C, sh_sumsq, s);
+                shard_allreduce(sh, sh_sumsq, C, s);
+                launch_wide_normalize_by(Um[n], t->dims[n], C, sh_sumsq, lam, s);
+                launch_wide_gram(Um[n], t->dims[n], C, Gn, s);
+            } else {
+                launch_col_sumsq(Um[n], t->dims[n], C, sh_sumsq, s);
+                shard_allreduce(sh, sh_sumsq, C, s);
+                launch_normalize_cols_by(Um[n], t->dims[n], C, sh_sumsq, lam, s);
+                launch_gram(Um[n], t->dims[n], C, Gn, s);
+            }
             count_launch(3);
             check_launch("als_update_sharded");
             shard_allreduce(sh, Gn, static_cast<long long>(C) * C, s);
@@ -2522,7 +2562,19 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             for (int k = hsplit; k < N; ++k) steps.push_back({[&, k] { half_step(k, hsplit, N); }, k});
         }
         auto fit_step = [&]() {
-            if (sh) {  // <X, Y> summed over the shards
+            const double* Glast = grams + static_cast<long long>(N - 1) * C * C;
+            if (wide) {
+                if (sh) {
+                    launch_wide_fit(Um[N - 1], fitM, t->dims[N - 1], C, lam, H, Glast, dnorm, fitb, nullptr, sh_inner,
+                                    s);
+                    shard_allreduce(sh, sh_inner, 1, s);
+                    launch_wide_fit(nullptr, nullptr, 0, C, lam, H, Glast, dnorm, fitb, sh_inner, nullptr, s);
+                    count_launch(1);
+                } else {
+                    launch_wide_fit(Um[N - 1], fitM, t->dims[N - 1], C, lam, H, Glast, dnorm, fitb, nullptr, nullptr,
+                                    s);
+                }
+            } else if (sh) {  // <X, Y> summed over the shards
                 launch_fit_inner(Um[N - 1], fitM, t->dims[N - 1], C, lam, sh_inner, s);
                 shard_allreduce(sh, sh_inner, 1, s);
                 launch_fit_from_inner(lam, C, H, grams + static_cast<long long>(N - 1) * C * C, dnorm, sh_inner, fitb,
@@ -2807,7 +2859,6 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
         const long long C = nfactors > 0 ? factor_cols[0] : 0;
         if (nlambda != C) fail(DMTK_GPU_EINVAL, "model lambda length does not match rank");
         validate_factors(t, nfactors, factors, factor_rows, factor_cols, N - 1, threads, "mttkrp");
-        if (C > 64) fail(DMTK_GPU_EINVAL, "fit: rank above 64 is not supported on the GPU path");
         Context& ctx = context(t->device);
         std::lock_guard<std::recursive_mutex> lk(ctx.mu);
         CK(cudaSetDevice(t->device));
@@ -2817,18 +2868,29 @@ int dmtk_gpu_fit(dmtk_gpu_tensor t, int nfactors, const double* const* factors, 
         upload_factors(ctx, *t, factors, C, dptr);
         const long long rows = t->dims[N - 1];
         ctx.out.ensure(static_cast<size_t>(rows * C));
-        ctx.als_small.ensure(64 * 64 + 64 + 8);
+        const long long CM = std::max<long long>(C, 64);
+        ctx.als_small.ensure(static_cast<size_t>(CM * CM + CM + 16 + (C > 64 ? N * C * C : 0)));
         double* H = ctx.als_small.p;
-        double* lam = H + 64 * 64;
-        double* dn = lam + 64;
+        double* lam = H + CM * CM;
+        double* dn = lam + CM;
         double* o4 = dn + 1;
         CK(cudaMemcpyAsync(lam, lambda, static_cast<size_t>(C) * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
         CK(cudaMemcpyAsync(dn, &normx, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
         // cp_als.cpp:160-172: last-mode one_step MTTKRP, then the fit formula
         mttkrp_enqueue(*t, ctx, dptr.data(), static_cast<int>(C), N - 1, DMTK_GPU_ONE_STEP, 0, ctx.out.p, ctx.stream,
                        nullptr);
-        gram_hadamard_dev(ctx, t->dims, dptr, static_cast<int>(C), N - 1, H, ctx.stream);
-        launch_fit(dptr[N - 1], ctx.out.p, rows, static_cast<int>(C), lam, H, dn, o4, ctx.stream);
+        if (C > 64) {  // Grams of every factor, their Hadamard product, the fit (als_wide.cu)
+            double* grams = o4 + 8;
+            for (int k = 0; k < N; ++k)
+                launch_wide_gram(dptr[k], t->dims[k], static_cast<int>(C), grams + k * C * C, ctx.stream);
+            launch_wide_hadamard(grams, N, static_cast<int>(C), N - 1, H, ctx.stream);
+            launch_wide_fit(dptr[N - 1], ctx.out.p, rows, static_cast<int>(C), lam, H, grams + (N - 1) * C * C, dn, o4,
+                            nullptr, nullptr, ctx.stream);
+            count_launch(N + 1);
+        } else {
+            gram_hadamard_dev(ctx, t->dims, dptr, static_cast<int>(C), N - 1, H, ctx.stream);
+            launch_fit(dptr[N - 1], ctx.out.p, rows, static_cast<int>(C), lam, H, dn, o4, ctx.stream);
+        }
         check_launch("fit");
         CK(cudaMemcpyAsync(out4, o4, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
         CK(cudaStreamSynchronize(ctx.stream));

@@ -97,6 +97,21 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s);
 
+// als_wide.cu: the CP-ALS update for ranks above 64 (global-memory systems)
+long long wide_scratch_doubles(int C, long long max_rows);
+void launch_wide_gram(const double* U, long long rows, int C, double* G, cudaStream_t s);
+void launch_wide_hadamard(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s);
+int launch_wide_solve(const double* H, int C, const double* M, long long rows, double* U, double* scratch, int* flag,
+                      cudaStream_t s);
+void launch_wide_col_sumsq(const double* U, long long rows, int C, double* sumsq, cudaStream_t s);
+void launch_wide_normalize_by(double* U, long long rows, int C, const double* sumsq, double* lambda, cudaStream_t s);
+int launch_wide_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M,
+                           long long rows, double* U, double* lambda, double* Gn, double* scratch, double* sumsq,
+                           int* flag, cudaStream_t s, bool solve_only);
+void launch_wide_fit(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
+                     const double* Hlast, const double* Glast, const double* normx, double* out, const double* inner_in,
+                     double* inner_out, cudaStream_t s);
+
 // Tensor-core streaming MTTKRP (mttkrp_tc.cuh). nb in [1, 8], tail in
 // {0, 1, 2, 4}, rb (row blocks per warp, p.RB) in {2, 3, 4}; returns false /
 // -1 when no instantiation matches.

@@ -241,3 +241,51 @@ def test_pack_symmetric_validation(oracle):
     f = oracle.gen_factors(dims, 2, 1)
     with pytest.raises(dg.InvalidArgument):  # packed handles only run cp_als / tensor_norm
         dg.mttkrp(dg.MttkrpRequest(tp, f, 0))
+
+
+# ----------------------------------------------------------- ranks above 64
+@pytest.mark.parametrize("dims,rank", [((90, 85, 80), 72), ((70, 66, 8, 9), 100)])
+def test_cp_als_rank_above_64_matches_reference(ref, oracle, dims, rank):
+    """The reference takes any rank >= 1 (cp_als.cpp:175-177): ranks above 64
+    run the per-mode sweep with the global-memory factor update (als_wide.cu:
+    left-looking Cholesky + row substitution, the Jacobi fallback)."""
+    x = oracle.gen_tensor(dims, 31)
+    got = cp(x, dims, rank, 6, 7)
+    want = ref.cp_als(x, dims, rank, 6, tol=0.0, seed=7)
+    f_got = np.array([r.fit.fit for r in got.trace.iters])
+    assert np.max(np.abs(f_got - want["fits"])) <= 1e-9
+    for u, v in zip(got.model.factors, want["factors"]):
+        assert np.linalg.norm(u - v) <= 1e-6 * np.linalg.norm(v)
+    t = dg.DenseTensor(dims, x)
+    fr = dg.fit(t, got.model)
+    rf = ref.fit(x, dims, got.model.factors, got.model.lambda_)
+    assert abs(fr.fit - rf["fit"]) <= 1e-9
+    with pytest.raises(dg.InvalidArgument):
+        dg.cp_als(t, AlsConfig(rank=rank, max_iters=2, tol=0.0, seed=7, dimension_tree=True))
+
+
+def test_gram_hadamard_and_solve_rank_above_64(ref, oracle):
+    f = oracle.gen_factors((120, 110, 100), 96, 5)
+    h = dg.gram_hadamard(f, 1)
+    want = ref.gram_hadamard(f, 1)
+    assert np.linalg.norm(h - want) <= 1e-13 * np.linalg.norm(want)
+    m = oracle.gen_factors((300,), 96, 6)[0]
+    u = dg.solve_psd(h, m)
+    assert np.linalg.norm(u - ref.solve_psd(h, m)) <= 1e-8 * np.linalg.norm(u)
+    # a singular system (rank-deficient Gram): the Jacobi pseudo-inverse path
+    g = oracle.gen_factors((40,), 80, 7)[0]
+    hs = g.T @ g
+    us = dg.solve_psd(hs, m[:, :80].copy())
+    ws = ref.solve_psd(hs, m[:, :80].copy())
+    assert np.linalg.norm(us - ws) <= 1e-6 * np.linalg.norm(ws)
+
+
+@pytest.mark.timeout(300)
+def test_loopback_sharded_rank_above_64(oracle, ref):
+    from paper_1708_08976_b200.distributed import loopback_cp_als
+    dims, rank = (70, 66, 9, 10), 80
+    x = oracle.gen_tensor(dims, 3)
+    t = dg.DenseTensor(dims, x)
+    res, _ = loopback_cp_als(t, 3, AlsConfig(rank=rank, max_iters=4, tol=0.0, seed=2))
+    want = ref.cp_als(x, dims, rank, 4, tol=0.0, seed=2)
+    assert np.max(np.abs(np.array(res[0].fits) - want["fits"])) <= 1e-9
