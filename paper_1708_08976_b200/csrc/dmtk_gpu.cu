@@ -898,44 +898,73 @@ struct TuneChoice {
     int rb = 0;        // tile height RB forced (0 = the modelled one)
 };
 static std::mutex g_tune_mu;
-static std::map<TuneKey, TuneChoice> g_tune;
+static std::map<TuneKey, TuneChoice> g_tune;      // this process's and the user file's decisions
+static std::map<TuneKey, TuneChoice> g_tune_pkg;  // the packaged table (tune_b200.txt)
+static int g_tune_pkg_sms = -1;                   // the SM count the packaged table was measured on
 constexpr long long kTuneBytes = 256LL << 20;
 
-// DMTK_GPU_TUNE_CACHE=<file>: decisions persist across processes (one line
-// per key: ndim dims... mode C aligned s bj1 rb), read on first use and appended
-// on every new decision -- e.g. so a profiler run, whose serialised launches
-// would distort the timing, replays the plain run's choices.
+// Decision files: one line per key "ndim dims... mode C aligned s bj1 rb".
+//  * tune_b200.txt next to this library: decisions measured on a B200 for the
+//    BASELINE shapes (tools/make_tune_table.py), header "# sms <count>"; used
+//    only on a device with that SM count. Results are then a function of the
+//    shape alone, the same in every process.
+//  * DMTK_GPU_TUNE_CACHE=<file>: read on first use and appended with every
+//    new measured decision (e.g. a profiler run replays a plain run's choices).
 static const char* tune_cache_path() {
     static const char* p = std::getenv("DMTK_GPU_TUNE_CACHE");
     return p && *p ? p : nullptr;
+}
+static void tune_read(const char* path, std::map<TuneKey, TuneChoice>& into, int* sms) {
+    FILE* f = std::fopen(path, "r");
+    if (!f) return;
+    char line[4096];
+    while (std::fgets(line, sizeof line, f)) {
+        if (line[0] == '#') {
+            if (sms) std::sscanf(line, "# sms %d", sms);
+            continue;
+        }
+        std::vector<long long> v;
+        char* p = line;
+        char* end = nullptr;
+        for (long long x = std::strtoll(p, &end, 10); end != p; x = std::strtoll(p, &end, 10)) {
+            v.push_back(x);
+            p = end;
+        }
+        if (v.empty() || v[0] < 1 || v[0] > 64 || static_cast<long long>(v.size()) != v[0] + 7) continue;
+        TuneKey k;
+        k.pdims.assign(v.begin() + 1, v.begin() + 1 + v[0]);
+        const long long* r = v.data() + 1 + v[0];
+        k.mode = static_cast<int>(r[0]);
+        k.C = static_cast<int>(r[1]);
+        k.aligned = r[2] != 0;
+        into[k] = TuneChoice{static_cast<int>(r[3]), r[4] != 0, static_cast<int>(r[5])};
+    }
+    std::fclose(f);
 }
 static void tune_load_locked() {
     static bool loaded = false;
     if (loaded) return;
     loaded = true;
-    const char* path = tune_cache_path();
-    if (!path) return;
-    FILE* f = std::fopen(path, "r");
-    if (!f) return;
-    int nd;
-    while (std::fscanf(f, "%d", &nd) == 1 && nd > 0 && nd <= 64) {
-        TuneKey k;
-        k.pdims.resize(nd);
-        bool ok = true;
-        for (auto& d : k.pdims) ok = ok && std::fscanf(f, "%lld", &d) == 1;
-        int al = 0, sv = 0, bj = 0, rb = 0;
-        ok = ok && std::fscanf(f, "%d %d %d %d %d %d", &k.mode, &k.C, &al, &sv, &bj, &rb) == 6;
-        if (!ok) break;
-        k.aligned = al != 0;
-        g_tune[k] = TuneChoice{sv, bj != 0, rb};
+    Dl_info info;
+    if (dladdr(reinterpret_cast<void*>(&tune_read), &info) && info.dli_fname) {
+        std::string dir(info.dli_fname);
+        const size_t slash = dir.rfind('/');
+        dir = slash == std::string::npos ? std::string(".") : dir.substr(0, slash);
+        tune_read((dir + "/tune_b200.txt").c_str(), g_tune_pkg, &g_tune_pkg_sms);
     }
-    std::fclose(f);
+    if (const char* path = tune_cache_path()) tune_read(path, g_tune, nullptr);
 }
-static bool tune_lookup(const TuneKey& k, TuneChoice& c) {
+static bool tune_lookup(const TuneKey& k, TuneChoice& c, int sms) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     tune_load_locked();
     auto it = g_tune.find(k);
-    if (it == g_tune.end()) return false;
+    if (it != g_tune.end()) {
+        c = it->second;
+        return true;
+    }
+    if (sms != g_tune_pkg_sms) return false;
+    it = g_tune_pkg.find(k);
+    if (it == g_tune_pkg.end()) return false;
     c = it->second;
     return true;
 }
@@ -951,10 +980,13 @@ static void tune_store(const TuneKey& k, const TuneChoice& c) {
         }
     }
 }
+// Measuring is opt-in (DMTK_GPU_AUTOTUNE=1): by default a shape takes the
+// packaged / cached decision or the cost model's pick, so results never
+// depend on timings (the same bytes in every process).
 static bool tune_enabled(const dmtk_gpu_tensor_s& t, cudaStream_t s, bool* deferred = nullptr) {
     static const bool off = [] {
         const char* e = std::getenv("DMTK_GPU_AUTOTUNE");
-        return e && std::string(e) == "0";
+        return !(e && std::string(e) == "1");
     }();
     static const long long min_bytes = [] {  // DMTK_GPU_TUNE_BYTES: threshold override (tests)
         const char* e = std::getenv("DMTK_GPU_TUNE_BYTES");
@@ -1139,10 +1171,12 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                     // Large tensors: the modelled choice misses DRAM effects (K-major
                     // tiles whose rows lie megabytes apart stream at ~4.5 TB/s), so
                     // the candidates are timed once per shape and the fastest kept
-                    if (force_s == 0 && tune_enabled(t, s, &tune_deferred)) {
-                        const TuneKey tk{t.pdims, mode, C, t.d != nullptr && (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
-                        TuneChoice tc;
-                        if (!tune_lookup(tk, tc)) {
+                    const TuneKey tk{t.pdims, mode, C, t.d != nullptr && (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
+                    TuneChoice tc;
+                    bool have = force_s == 0 && tune_lookup(tk, tc, ctx.sms);
+                    if (force_s == 0 && !have && tune_enabled(t, s, &tune_deferred)) {
+                        have = true;
+                        {
                             std::vector<std::pair<ModePlan, TuneChoice>> cands{{one_step, {0, false}}};
                             for (int sp = 1; sp <= N - 2; ++sp)
                                 for (bool bj1 : {false, true}) {
@@ -1185,6 +1219,8 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                             tc = picks[pick_fastest(runs, modelled, s)];
                             tune_store(tk, tc);
                         }
+                    }
+                    if (have) {
                         pre = tc.s == 0 && tc.rb == 0 ? one_step : view_of(tc);
                         best_s = tc.s;
                     }
@@ -1238,16 +1274,17 @@ static void mttkrp_enqueue_core(dmtk_gpu_tensor_s& t, Context& ctx, const double
                 ModePlan chosen = left ? pl : pr;
                 // large tensors: time the two orders (and the left order with
                 // BJ = 1 row tiles) once per shape, as for the boundary views
-                if (pr.kind != kGeneric && pl.kind != kGeneric && tune_enabled(t, s, &tune_deferred)) {
-                    const TuneKey tk{t.pdims, mode, C, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
-                    TuneChoice tc;
+                const TuneKey tk{t.pdims, mode, C, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
+                TuneChoice tc;
+                bool have = pr.kind != kGeneric && pl.kind != kGeneric && tune_lookup(tk, tc, ctx.sms);
+                if (pr.kind != kGeneric && pl.kind != kGeneric && (have || tune_enabled(t, s, &tune_deferred))) {
                     const ModePlan pl1 = plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C, kTcKJ,
                                                    0, ctx.sms, true);
                     auto order_view = [&](const TuneChoice& c) {
                         return plan_view(prod(dims, 0, mode), dims[mode], prod(dims, mode + 1, N), C,
                                          c.s == DMTK_GPU_ORDER_RIGHT ? kTcM : kTcKJ, 0, ctx.sms, c.bj1, c.rb);
                     };
-                    if (!tune_lookup(tk, tc)) {
+                    if (!have) {
                         const KrpGen gr_b = make_gen(dims, mode + 1, N, dU, C, ones), gr_s = make_gen(dims, 0, mode, dU, C, ones);
                         const KrpGen gl_b = gr_s, gl_s = gr_b;
                         std::vector<std::pair<ModePlan, TuneChoice>> cands{{pr, {DMTK_GPU_ORDER_RIGHT, false}},

@@ -151,7 +151,7 @@ def test_measured_view_selection():
     once per shape (tune_enabled, dmtk_gpu.cu). The size threshold is lowered
     to 0 here so the timed selection, and the one-output-row epilogue
     instantiation (kEpiSwr) of its BJ = 1 candidates, run on small shapes."""
-    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0")
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0", DMTK_GPU_AUTOTUNE="1")
     shapes = ["40x40x12x8:20", "100x10x30x8:25", "8x60x50:16", "64x4x4x64:32", "9x11x13:20", "30x20x10x8:16",
               "300x40x40:25", "20x30x600:9"]
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
@@ -180,7 +180,7 @@ def test_tune_cache_file(tmp_path):
     second one reads and replays them (no retiming); results stay in
     tolerance either way."""
     cache = tmp_path / "tune.txt"
-    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0", DMTK_GPU_TUNE_CACHE=str(cache))
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0", DMTK_GPU_AUTOTUNE="1", DMTK_GPU_TUNE_CACHE=str(cache))
     shapes = ["300x40x40:25", "40x40x12x8:20"]
     for _ in range(2):
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
@@ -201,8 +201,37 @@ def test_measured_selection_random_shapes():
         n = int(rng.integers(3, 6))
         dims = [int(rng.integers(2, 40 if n == 3 else 14)) for _ in range(n)]
         shapes.append("x".join(map(str, dims)) + ":" + str(int(rng.integers(1, 41))))
-    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0")
+    env = dict(os.environ, DMTK_GPU_TUNE_BYTES="0", DMTK_GPU_AUTOTUNE="1")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+
+
+CROSS = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1708_08976_b200 as dg
+from paper_1708_08976_b200 import MttkrpAlgo as A, TwoStepOrder as O
+dims, C = (512, 384, 400), 20
+t = dg.DenseTensor.generate(dims, 3)
+fs = [f.download().reshape(d, C) for f, d in zip(dg.generate_factors(dims, C, 4), dims)]
+res = [dg.mttkrp(dg.MttkrpRequest(t, fs, m)).m for m in range(3)]
+res.append(dg.mttkrp(dg.MttkrpRequest(t, fs, 1, A.two_step)).m)
+np.save({out!r}, np.stack([r.reshape(-1)[:7680] for r in res]))
+"""
+
+
+def test_results_identical_across_processes(tmp_path):
+    """The same call in two processes returns the same bytes (a 600 MB
+    tensor, above the measured-selection threshold): by default the view of a
+    boundary mode and the 2-step order come from the packaged decision table or
+    the cost model, never from a timing."""
+    outs = []
+    for k in range(2):
+        out = str(tmp_path / f"r{k}.npy")
+        r = subprocess.run([sys.executable, "-c", CROSS.format(root=ROOT, out=out)], capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
