@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -62,6 +64,41 @@ __device__ __forceinline__ double krp_head(const KrpGen& g, long long idx, int c
         v *= __ldg(g.U[f] + krp_digit(g, f, idx) * g.ldu + c);
     }
     return v;
+}
+
+// ------------------------------------------- programmatic dependent launch
+// Kernels launched with launch_pdl may start while the previous kernel in the
+// stream finishes (its launch latency and prologue overlap that kernel's
+// tail). Every such kernel calls pdl_wait() before it reads anything an
+// earlier kernel wrote (and before it writes anything an earlier kernel
+// reads), then pdl_trigger() -- always after the wait, so a chain of early
+// launches never overtakes a kernel that is still running two launches back.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// DMTK_GPU_NO_PDL=1: plain launches (A/B switch)
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DMTK_GPU_NO_PDL");
+        return !(e && *e && *e != '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(std::forward<Args>(args))...);
 }
 
 // ---------------------------------------------------------------- mbarrier

@@ -802,6 +802,7 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         }
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
         mp.tc.X = X;
+        mp.tc.x_wait = X != t.d;  // a scratch copy (baseline matricisation) may still be in flight
         static const bool force_ldgsts = std::getenv("DMTK_GPU_FORCE_LDGSTS") != nullptr;
         if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || force_ldgsts) mp.tc.ldgsts = 1;
         static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;

@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
                                                                      const long long* __restrict__ slots, int C,
                                                                      double* __restrict__ out) {
     __shared__ double part[kReduceThreads];
+    pdl_wait();  // the slots are the streaming kernel's output
+    pdl_trigger();
     const long long i = blockIdx.x;
     const int P = kReduceThreads / C;
     const int p = threadIdx.x / C;
@@ -275,6 +277,8 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
 __global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
                                         const long long* __restrict__ slots, long long rows, int C,
                                         double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= rows * C) return;
     const long long i = e / C;
@@ -1113,11 +1117,12 @@ void launch_slot_reduce(const double* ws, const long long* rowptr, const long lo
     if (rows <= 0) return;
     if (nslots <= 8 * rows) {  // a few slots per row: one thread per (row, column), rows in order
         const long long n = rows * C;
-        slot_reduce_thin_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, rowptr, slots, rows, C,
-                                                                                       out);
+        launch_pdl(slot_reduce_thin_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, ws, rowptr,
+                   slots, rows, C, out);
         return;
     }
-    slot_reduce_kernel<<<static_cast<unsigned>(rows), kReduceThreads, 0, s>>>(ws, rowptr, slots, C, out);
+    launch_pdl(slot_reduce_kernel, dim3(static_cast<unsigned>(rows)), dim3(kReduceThreads), 0, s, ws, rowptr, slots, C,
+               out);
 }
 
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s) {

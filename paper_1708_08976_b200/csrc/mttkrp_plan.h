@@ -80,6 +80,8 @@ struct TcPlan {
                               // copies the swizzled stage with 8-byte cp.async instead
     int epi;                  // epilogue instantiation (Epi): kEpiGen compiles every flavor's epilogue,
                               // the others only their own (fewer live registers in the consumer loop)
+    int x_wait;               // 1: X is a scratch buffer an earlier kernel wrote (the baseline's
+                              // matricised copy): the producer waits for it too (pdl_wait)
 };
 
 // Epilogue instantiations of the streaming kernel (template parameter EPI).

@@ -122,6 +122,15 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     }
     if (warp == kProducerWarp && lane == 0 && !p.ldgsts) tma_prefetch_desc(&tmap);
     __syncthreads();
+    // Programmatic dependent launch: the producer streams X (never written by
+    // the library's kernels) without waiting for the previous kernel unless X
+    // is a buffer that kernel may have just produced (x_wait); the builders
+    // (factor rows) and the consumers (workspace slots, read by the previous
+    // call's reduction) wait for it.
+    if (warp != kProducerWarp || p.x_wait) {
+        pdl_wait();
+        pdl_trigger();
+    }
 
     long long lo, hi;
     cta_stage_range(p.total_stages, gridDim.x, blockIdx.x, lo, hi);

@@ -26,7 +26,7 @@ static void launch_one(const TcPlan& p, const CUtensorMap& map, int grid, cudaSt
         auto k = mttkrp_tc_kernel<TC_NB, TAIL, KM, TC_RB, EPI>;
         static std::atomic<unsigned long long> opted{0};  // per device; not a stream op (graph-safe)
         once_on_device(opted, [k] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
-        k<<<grid, tc_threads(TC_RB), p.smem, s>>>(map, p);
+        launch_pdl(k, dim3(grid), dim3(tc_threads(TC_RB)), p.smem, s, map, p);
     }
 }
 
