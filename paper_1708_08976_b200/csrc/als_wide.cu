@@ -39,6 +39,8 @@ __device__ double block_sum(double v, double* red) {
 
 // G = U^T U (rows x C), one thread per entry, rows in order
 __global__ void wide_gram_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ G) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= static_cast<long long>(C) * C) return;
     const int c1 = static_cast<int>(e / C), c2 = static_cast<int>(e % C);
@@ -50,6 +52,8 @@ __global__ void wide_gram_kernel(const double* __restrict__ U, long long rows, i
 // H = Hadamard of the cached Grams of every mode but `skip`
 __global__ void wide_hadamard_kernel(const double* __restrict__ grams, int nmodes, int C, int skip,
                                      double* __restrict__ H) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long cc = static_cast<long long>(C) * C;
     if (e >= cc) return;
@@ -65,6 +69,8 @@ __global__ void wide_hadamard_kernel(const double* __restrict__ grams, int nmode
 // falls to 1e-12 * trace or below.
 __global__ void __launch_bounds__(kT) wide_cholesky_kernel(const double* __restrict__ H, int n, double* __restrict__ L,
                                                            int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[33];
     __shared__ double s_root;
     __shared__ int s_ok;
@@ -109,6 +115,8 @@ __global__ void __launch_bounds__(kT) wide_cholesky_kernel(const double* __restr
 // (linalg.cpp:340-354), y kept in the output row. One thread per row.
 __global__ void wide_chol_rows_kernel(const double* __restrict__ L, int n, const double* __restrict__ M, long long rows,
                                       double* __restrict__ U, const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (!flag[0]) return;
     const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= rows) return;
@@ -132,6 +140,8 @@ __global__ void wide_chol_rows_kernel(const double* __restrict__ L, int n, const
 __global__ void __launch_bounds__(kT) wide_jacobi_kernel(const double* __restrict__ H, int n, double* __restrict__ a,
                                                          double* __restrict__ v, double* __restrict__ gain,
                                                          const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (flag[0]) return;
     __shared__ double red[33];
     __shared__ double s_cs, s_sn;
@@ -207,6 +217,8 @@ __global__ void __launch_bounds__(kT) wide_jacobi_kernel(const double* __restric
 __global__ void wide_jacobi_rows_kernel(const double* __restrict__ V, const double* __restrict__ gain, int n,
                                         const double* __restrict__ M, long long rows, double* __restrict__ tmp,
                                         double* __restrict__ U, const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (flag[0]) return;
     const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= rows) return;
@@ -227,6 +239,8 @@ __global__ void wide_jacobi_rows_kernel(const double* __restrict__ V, const doub
 // Column sums of squares, one CTA per column (fixed order)
 __global__ void __launch_bounds__(kT) wide_col_sumsq_kernel(const double* __restrict__ U, long long rows, int C,
                                                             double* __restrict__ sumsq) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[33];
     const int c = blockIdx.x;
     double sq = 0.0;
@@ -239,6 +253,8 @@ __global__ void __launch_bounds__(kT) wide_col_sumsq_kernel(const double* __rest
 // (normalize_mode, cp_als.cpp:101-118)
 __global__ void wide_normalize_by_kernel(double* __restrict__ U, long long rows, int C,
                                          const double* __restrict__ sumsq, double* __restrict__ lambda) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long c = e % C;
     const double nrm = sqrt(sumsq[c]);
@@ -256,6 +272,8 @@ __global__ void __launch_bounds__(kT) wide_fit_kernel(const double* __restrict__
                                                       const double* __restrict__ normx, double* __restrict__ out,
                                                       const double* __restrict__ inner_in,
                                                       double* __restrict__ inner_out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[33];
     double inner = 0.0;
     if (!inner_in)
@@ -297,11 +315,11 @@ long long wide_scratch_doubles(int C, long long max_rows) {
 }
 
 void launch_wide_gram(const double* U, long long rows, int C, double* G, cudaStream_t s) {
-    wide_gram_kernel<<<blocks_for(static_cast<long long>(C) * C, 128), 128, 0, s>>>(U, rows, C, G);
+    launch_pdl(wide_gram_kernel, dim3(blocks_for(static_cast<long long>(C) * C, 128)), dim3(128), 0, s, U, rows, C, G);
 }
 
 void launch_wide_hadamard(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s) {
-    wide_hadamard_kernel<<<blocks_for(static_cast<long long>(C) * C, 256), 256, 0, s>>>(grams, nmodes, C, skip, H);
+    launch_pdl(wide_hadamard_kernel, dim3(blocks_for(static_cast<long long>(C) * C, 256)), dim3(256), 0, s, grams, nmodes, C, skip, H);
 }
 
 // solve_psd for any rank: scratch = wide_scratch_doubles(C, rows)
@@ -312,20 +330,20 @@ int launch_wide_solve(const double* H, int C, const double* M, long long rows, d
     double* V = a + static_cast<long long>(C) * C;
     double* gain = V + static_cast<long long>(C) * C;
     double* tmp = gain + C;
-    wide_cholesky_kernel<<<1, kT, 0, s>>>(H, C, L, flag);
-    wide_chol_rows_kernel<<<blocks_for(rows, 128), 128, 0, s>>>(L, C, M, rows, U, flag);
-    wide_jacobi_kernel<<<1, kT, 0, s>>>(H, C, a, V, gain, flag);
-    wide_jacobi_rows_kernel<<<blocks_for(rows, 128), 128, 0, s>>>(V, gain, C, M, rows, tmp, U, flag);
+    launch_pdl(wide_cholesky_kernel, dim3(1), dim3(kT), 0, s, H, C, L, flag);
+    launch_pdl(wide_chol_rows_kernel, dim3(blocks_for(rows, 128)), dim3(128), 0, s, L, C, M, rows, U, flag);
+    launch_pdl(wide_jacobi_kernel, dim3(1), dim3(kT), 0, s, H, C, a, V, gain, flag);
+    launch_pdl(wide_jacobi_rows_kernel, dim3(blocks_for(rows, 128)), dim3(128), 0, s, V, gain, C, M, rows, tmp, U, flag);
     return 4;
 }
 
 void launch_wide_col_sumsq(const double* U, long long rows, int C, double* sumsq, cudaStream_t s) {
-    wide_col_sumsq_kernel<<<C, kT, 0, s>>>(U, rows, C, sumsq);
+    launch_pdl(wide_col_sumsq_kernel, dim3(C), dim3(kT), 0, s, U, rows, C, sumsq);
 }
 
 void launch_wide_normalize_by(double* U, long long rows, int C, const double* sumsq, double* lambda, cudaStream_t s) {
     const long long n = rows * C > C ? rows * C : C;
-    wide_normalize_by_kernel<<<blocks_for(n, 256), 256, 0, s>>>(U, rows, C, sumsq, lambda);
+    launch_pdl(wide_normalize_by_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, s, U, rows, C, sumsq, lambda);
 }
 
 // One ALS factor update for any rank (the rank <= 64 launch_als_update's
@@ -346,7 +364,7 @@ int launch_wide_als_update(const double* grams, int nmodes, int C, int skip, dou
 void launch_wide_fit(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                      const double* Hlast, const double* Glast, const double* normx, double* out, const double* inner_in,
                      double* inner_out, cudaStream_t s) {
-    wide_fit_kernel<<<1, kT, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, Glast, normx, out, inner_in, inner_out);
+    launch_pdl(wide_fit_kernel, dim3(1), dim3(kT), 0, s, U, Mlast, rows, C, lambda, Hlast, Glast, normx, out, inner_in, inner_out);
 }
 
 }  // namespace dmtkg

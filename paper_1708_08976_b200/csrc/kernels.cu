@@ -25,6 +25,8 @@ namespace dmtkg {
 constexpr long long kKrpChunk = 4096;  // doubles per work unit (32 KB of output)
 __global__ void __launch_bounds__(256) krp_level_kernel(const double* __restrict__ P, const double* __restrict__ U,
                                                         double* __restrict__ out, long long Q, int J, int C) {
+    pdl_wait();
+    pdl_trigger();
     // Output rows q*J .. q*J + J - 1 form one contiguous J*C block equal to U
     // with column c scaled by P(q, c). Work units are 32 KB chunks of those
     // blocks (balanced over the grid whatever Q is); inside a unit every
@@ -95,6 +97,8 @@ __global__ void __launch_bounds__(256) krp_level_kernel(const double* __restrict
 __global__ void __launch_bounds__(256) multittv_partial_kernel(const double* __restrict__ P, int C, long long A,
                                                                long long dt, long long B, KrpGen kl, KrpGen kr,
                                                                long long per_chunk, double* __restrict__ ws) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[256];
     const long long i = blockIdx.x;
     const long long s = blockIdx.y;
@@ -137,6 +141,8 @@ __global__ void __launch_bounds__(256) multittv_partial_kernel(const double* __r
 
 __global__ void multittv_final_kernel(const double* __restrict__ ws, int S, long long dt, int C,
                                       double* __restrict__ M) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= dt * C) return;
     double t = 0.0;
@@ -153,6 +159,8 @@ __global__ void multittv_final_kernel(const double* __restrict__ ws, int S, long
 // flag = 1 if any X(i, j, r) != X(j, i, r) (exact comparison)
 __global__ void sym01_check_kernel(const double* __restrict__ X, long long I, long long pd0, long long R,
                                    int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     const long long per = I * I;
     for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < per * R;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -166,6 +174,8 @@ __global__ void sym01_check_kernel(const double* __restrict__ X, long long I, lo
 // Xp(p, r) = X(i, j, r), i <= j; one block per (r, j), threads over i
 __global__ void sym01_pack_kernel(const double* __restrict__ X, long long I, long long pd0, long long Pp,
                                   double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const long long r = blockIdx.x;
     const long long j = blockIdx.y;
     const double* src = X + pd0 * (j + I * r);
@@ -180,6 +190,8 @@ __global__ void sym01_pack_kernel(const double* __restrict__ X, long long I, lon
 // One block per a; thread (part, c) strides b, parts added in a fixed order.
 __global__ void __launch_bounds__(256) sym01_mttv_kernel(const double* __restrict__ Q, long long I, int C,
                                                          const double* __restrict__ V, double* __restrict__ M) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[256];
     const long long a = blockIdx.x;
     const int parts = blockDim.x / C;
@@ -204,6 +216,8 @@ __global__ void __launch_bounds__(256) sym01_mttv_kernel(const double* __restric
 // diagonal: the pair weights that replace the KRP rows of modes 0 and 1
 __global__ void sym01_pairs_kernel(const double* __restrict__ A, const double* __restrict__ B, long long I, int C,
                                    long long Pp, double* __restrict__ W) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= Pp * C) return;
     const long long p = e / C;
@@ -224,6 +238,8 @@ __global__ void sym01_pairs_kernel(const double* __restrict__ A, const double* _
 // Slot layout ws[(jc * I + i) * C + c]; the CSR reduce finishes the sum.
 __global__ void mttkrp_generic_kernel(const double* __restrict__ X, long long L, long long I, long long R, int C,
                                       KrpGen kl, KrpGen kr, long long jchunk, double* __restrict__ ws) {
+    pdl_wait();
+    pdl_trigger();
     const long long jc = blockIdx.x;
     const long long e = static_cast<long long>(blockIdx.y) * blockDim.x + threadIdx.x;
     if (e >= I * C) return;
@@ -252,6 +268,8 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
                                                                      const long long* __restrict__ rowptr,
                                                                      const long long* __restrict__ slots, int C,
                                                                      double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double part[kReduceThreads];
     pdl_wait();  // the slots are the streaming kernel's output
     pdl_trigger();
@@ -279,6 +297,8 @@ __global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const lon
                                         double* __restrict__ out) {
     pdl_wait();
     pdl_trigger();
+    pdl_wait();
+    pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= rows * C) return;
     const long long i = e / C;
@@ -293,6 +313,8 @@ __global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const lon
 // (mttkrp.cpp:272-290), done as a tiled transpose of every j-slab.
 __global__ void matricize_kernel(const double* __restrict__ X, long long L, long long I, long long R,
                                  double* __restrict__ dst) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double tile[32][33];
     const long long j = blockIdx.z;
     const long long l0 = static_cast<long long>(blockIdx.x) * 32;
@@ -314,6 +336,8 @@ __global__ void matricize_kernel(const double* __restrict__ X, long long L, long
 // order, mirrored so the result is symmetric to the last bit. Then H *= G.
 __global__ void gram_hadamard_accum_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ H,
                                            int first) {
+    pdl_wait();
+    pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= C * C) return;
     const int c1 = e / C, c2 = e % C;
@@ -326,6 +350,8 @@ __global__ void gram_hadamard_accum_kernel(const double* __restrict__ U, long lo
 }
 
 __global__ void fill_kernel(double* p, long long n, double v) {
+    pdl_wait();
+    pdl_trigger();
     for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
          e += static_cast<long long>(gridDim.x) * blockDim.x)
         p[e] = v;
@@ -334,6 +360,8 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // Cholesky with pivot floor 1e-12 * trace (linalg.cpp:254-276), one CTA.
 // Writes L (row-major, lower) and flag[0] = 1 on success, 0 on failure.
 __global__ void cholesky_kernel(const double* __restrict__ H, int n, double* __restrict__ Lm, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     // one warp; H and L staged in shared memory. Same operation order as the
     // reference (linalg.cpp:250-279): d = H_jj - sum_k L_jk^2 ascending in k,
     // then column j below the diagonal.
@@ -404,6 +432,8 @@ template <int NP>
 __global__ void __launch_bounds__(64) chol_solve_rows_kernel(const double* __restrict__ Lm, int n,
                                                              const double* __restrict__ M, long long rows,
                                                              double* __restrict__ U, const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (!flag[0]) return;
     __shared__ double sL[NP * NP];
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) sL[e] = Lm[e];
@@ -420,6 +450,8 @@ __global__ void __launch_bounds__(64) chol_solve_rows_kernel(const double* __res
 // ALS loop (cp_als); dmtk_gpu_solve_psd keeps the reference's substitution.
 __global__ void cholesky_inverse_kernel(const double* __restrict__ H, int n, double* __restrict__ Hinv,
                                         int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double shm[];
     double* sL = shm;
     double* sLi = shm + n * n;
@@ -480,6 +512,8 @@ __global__ void cholesky_inverse_kernel(const double* __restrict__ H, int n, dou
 // cache (measured 35 us against 15).
 __global__ void __launch_bounds__(32) cholesky_inverse_rl_kernel(const double* __restrict__ H, int n,
                                                                  double* __restrict__ Hinv, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int LDA = 33;
     __shared__ double A[32 * LDA];  // lower triangle becomes L
     __shared__ double X[32 * LDA];  // X[j][c] = L^-1[j][c]
@@ -548,6 +582,8 @@ __global__ void __launch_bounds__(32) cholesky_inverse_rl_kernel(const double* _
 __global__ void __launch_bounds__(256) als_solve_kernel(const double* __restrict__ grams, int nmodes, int skip, int n,
                                                         double* __restrict__ Hout, double* __restrict__ Hinv,
                                                         int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int LDA = 33;
     __shared__ double A[32 * LDA];
     __shared__ double X[32 * LDA];
@@ -626,6 +662,8 @@ __global__ void __launch_bounds__(256) als_solve_kernel(const double* __restrict
 __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restrict__ grams, int nmodes, int skip,
                                                            int n, double* __restrict__ Hout,
                                                            double* __restrict__ Hinv, int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int LDA = 33;
     __shared__ double A[2][32 * LDA];
     __shared__ double s_tr;
@@ -682,6 +720,8 @@ __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restr
 // U = M H^-1, one output element per thread (H^-1 staged in shared memory).
 __global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, const double* __restrict__ M,
                                      long long rows, double* __restrict__ U, const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (!flag[0]) return;
     extern __shared__ double sHi[];
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) sHi[e] = Hinv[e];
@@ -700,6 +740,8 @@ __global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, con
 // CTA; only runs when the Cholesky flag is 0. Produces V and gain.
 __global__ void jacobi_kernel(const double* __restrict__ H, int n, double* __restrict__ Vout, double* __restrict__ gain,
                               const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (flag[0]) return;
     __shared__ double a[64 * 64];
     double* v = Vout;  // eigenvectors rotated in place in global memory
@@ -774,6 +816,8 @@ __global__ void jacobi_kernel(const double* __restrict__ H, int n, double* __res
 __global__ void jacobi_apply_rows_kernel(const double* __restrict__ V, const double* __restrict__ gain, int n,
                                          const double* __restrict__ M, long long rows, double* __restrict__ U,
                                          const int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     if (flag[0]) return;
     const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= rows) return;
@@ -793,6 +837,8 @@ __global__ void jacobi_apply_rows_kernel(const double* __restrict__ V, const dou
 
 // Column norms into lambda, scale columns (cp_als.cpp:101-118). One CTA.
 __global__ void normalize_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double s_norm[64];
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         double sq = 0.0;
@@ -816,6 +862,8 @@ __global__ void normalize_kernel(double* __restrict__ U, long long rows, int C, 
 __global__ void fit_kernel(const double* __restrict__ U, const double* __restrict__ Mlast, long long rows, int C,
                            const double* __restrict__ lambda, const double* __restrict__ Hlast,
                            const double* __restrict__ normx, double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[256];
     __shared__ double G[64 * 64];
     double inner = 0.0;
@@ -861,6 +909,8 @@ __global__ void fit_kernel(const double* __restrict__ U, const double* __restric
 
 // Sum of squares, two passes, fixed reduction order (cp_als.cpp:21-30).
 __global__ void sumsq_partial_kernel(const double* __restrict__ x, long long n, double* __restrict__ part) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[512];
     double s0 = 0.0, s1 = 0.0;
     const long long n2 = n >> 1;
@@ -887,6 +937,8 @@ __global__ void sumsq_partial_kernel(const double* __restrict__ x, long long n, 
 }
 
 __global__ void sumsq_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out_norm) {
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int k = 0; k < n; ++k) s += part[k];
@@ -900,6 +952,8 @@ __global__ void sumsq_final_kernel(const double* __restrict__ part, int n, doubl
 // like linalg.cpp:210-226; deterministic run to run).
 __global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, int C, double* __restrict__ G,
                                  const int* __restrict__ only_if_failed) {
+    pdl_wait();
+    pdl_trigger();
     if (only_if_failed && only_if_failed[0]) return;
     int e = blockIdx.x, c1 = 0;
     while (e >= C - c1) {  // blockIdx -> (c1, c2 >= c1)
@@ -920,6 +974,8 @@ __global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, i
 // H = Hadamard of the cached Grams of every mode but `skip` (linalg.cpp:228-248).
 __global__ void hadamard_grams_kernel(const double* __restrict__ grams, int nmodes, int C, int skip,
                                       double* __restrict__ H) {
+    pdl_wait();
+    pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= C * C) return;
     double h = 1.0;
@@ -935,6 +991,8 @@ __global__ void hadamard_grams_kernel(const double* __restrict__ grams, int nmod
 __global__ void normalize_cols_kernel(double* __restrict__ U, long long rows, int C, double* __restrict__ lambda,
                                       const int* __restrict__ only_if_failed, double* __restrict__ sumsq_out = nullptr,
                                       const double* __restrict__ sumsq_in = nullptr) {
+    pdl_wait();
+    pdl_trigger();
     if (only_if_failed && only_if_failed[0]) return;
     __shared__ double red[256];
     __shared__ double s_norm;
@@ -973,6 +1031,8 @@ __global__ void fit_cached_kernel(const double* __restrict__ U, const double* __
                                   const double* __restrict__ Glast, const double* __restrict__ normx,
                                   double* __restrict__ out, const double* __restrict__ inner_in,
                                   double* __restrict__ inner_out) {
+    pdl_wait();
+    pdl_trigger();
     // inner_out: write <X, Y> of these rows and stop (a shard's partial);
     // inner_in: take <X, Y> from there (the partials summed over the shards)
     // <X, Y> from the last mode's MTTKRP and ||Y||^2 from the Grams, both as
@@ -1060,33 +1120,33 @@ void launch_krp_level(const double* P, const double* U, double* out, long long r
     const long long Q = rows_out / J;
     const long long units = Q * ((J * C + kKrpChunk - 1) / kKrpChunk);
     const long long blocks = std::min<long long>(units, 148LL * 8);
-    krp_level_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(P, U, out, Q,
+    launch_pdl(krp_level_kernel, dim3(static_cast<unsigned>(std::max<long long>(blocks, 1))), dim3(256), 0, s, P, U, out, Q,
                                                                                           static_cast<int>(J), C);
 }
 
 void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,
                            const KrpGen& kr, long long jchunk, long long n_jc, double* ws, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(n_jc), static_cast<unsigned>((I * C + 127) / 128));
-    mttkrp_generic_kernel<<<grid, 128, 0, s>>>(X, L, I, R, C, kl, kr, jchunk, ws);
+    launch_pdl(mttkrp_generic_kernel, dim3(grid), dim3(128), 0, s, X, L, I, R, C, kl, kr, jchunk, ws);
 }
 
 void launch_sym01_check(const double* X, long long I, long long pd0, long long R, int* flag, cudaStream_t s) {
-    sym01_check_kernel<<<148 * 8, 256, 0, s>>>(X, I, pd0, R, flag);
+    launch_pdl(sym01_check_kernel, dim3(148 * 8), dim3(256), 0, s, X, I, pd0, R, flag);
 }
 
 void launch_sym01_pack(const double* X, long long I, long long pd0, long long R, long long Pp, double* out,
                        cudaStream_t s) {
-    sym01_pack_kernel<<<dim3(static_cast<unsigned>(R), static_cast<unsigned>(I)), 128, 0, s>>>(X, I, pd0, Pp, out);
+    launch_pdl(sym01_pack_kernel, dim3(dim3(static_cast<unsigned>(R), static_cast<unsigned>(I))), dim3(128), 0, s, X, I, pd0, Pp, out);
 }
 
 void launch_sym01_mttv(const double* Q, long long I, int C, const double* V, double* M, cudaStream_t s) {
-    sym01_mttv_kernel<<<static_cast<unsigned>(I), 256, 0, s>>>(Q, I, C, V, M);
+    launch_pdl(sym01_mttv_kernel, dim3(static_cast<unsigned>(I)), dim3(256), 0, s, Q, I, C, V, M);
 }
 
 void launch_sym01_pairs(const double* A, const double* B, long long I, int C, long long Pp, double* W,
                         cudaStream_t s) {
     const long long n = Pp * C;
-    sym01_pairs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(A, B, I, C, Pp, W);
+    launch_pdl(sym01_pairs_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, A, B, I, C, Pp, W);
 }
 
 // chunks per output row: about eight 256-thread blocks per SM in all, each
@@ -1106,10 +1166,9 @@ void launch_multittv(const double* P, int C, long long A, long long dt, long lon
     const long long T = A * B;
     const long long S = multittv_chunks(A, dt, B);
     const long long per = (T + S - 1) / S;
-    multittv_partial_kernel<<<dim3(static_cast<unsigned>(dt), static_cast<unsigned>(S)), 256, 0, s>>>(
-        P, C, A, dt, B, kl, kr, per, ws);
+    launch_pdl(multittv_partial_kernel, dim3(dim3(static_cast<unsigned>(dt), static_cast<unsigned>(S))), dim3(256), 0, s, P, C, A, dt, B, kl, kr, per, ws);
     const long long n = dt * C;
-    multittv_final_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ws, static_cast<int>(S), dt, C, M);
+    launch_pdl(multittv_final_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, ws, static_cast<int>(S), dt, C, M);
 }
 
 void launch_slot_reduce(const double* ws, const long long* rowptr, const long long* slots, long long rows, int C,
@@ -1127,15 +1186,15 @@ void launch_slot_reduce(const double* ws, const long long* rowptr, const long lo
 
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>((I + 31) / 32), static_cast<unsigned>(R));
-    matricize_kernel<<<grid, dim3(32, 8), 0, s>>>(X, L, I, R, dst);
+    launch_pdl(matricize_kernel, dim3(grid), dim3(dim3(32, 8)), 0, s, X, L, I, R, dst);
 }
 
 void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s) {
-    gram_hadamard_accum_kernel<<<(C * C + 127) / 128, 128, 0, s>>>(U, rows, C, H, first ? 1 : 0);
+    launch_pdl(gram_hadamard_accum_kernel, dim3((C * C + 127) / 128), dim3(128), 0, s, U, rows, C, H, first ? 1 : 0);
 }
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {
-    fill_kernel<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
+    launch_pdl(fill_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, s, p, n, v);
 }
 
 void launch_solve_psd(const double* H, int n, const double* M, long long rows, double* U, double* scratch, int* flag,
@@ -1143,55 +1202,55 @@ void launch_solve_psd(const double* H, int n, const double* M, long long rows, d
     double* Lm = scratch;            // n*n
     double* V = scratch + 64 * 64;   // n*n
     double* gain = V + 64 * 64;      // n
-    cholesky_kernel<<<1, 32, 0, s>>>(H, n, Lm, flag);
+    launch_pdl(cholesky_kernel, dim3(1), dim3(32), 0, s, H, n, Lm, flag);
     const unsigned gs = static_cast<unsigned>((rows + 63) / 64);
     switch ((n + 7) / 8) {
-        case 1: chol_solve_rows_kernel<8><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 2: chol_solve_rows_kernel<16><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 3: chol_solve_rows_kernel<24><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 4: chol_solve_rows_kernel<32><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 5: chol_solve_rows_kernel<40><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 6: chol_solve_rows_kernel<48><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        case 7: chol_solve_rows_kernel<56><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
-        default: chol_solve_rows_kernel<64><<<gs, 64, 0, s>>>(Lm, n, M, rows, U, flag); break;
+        case 1: launch_pdl(chol_solve_rows_kernel<8>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 2: launch_pdl(chol_solve_rows_kernel<16>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 3: launch_pdl(chol_solve_rows_kernel<24>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 4: launch_pdl(chol_solve_rows_kernel<32>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 5: launch_pdl(chol_solve_rows_kernel<40>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 6: launch_pdl(chol_solve_rows_kernel<48>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        case 7: launch_pdl(chol_solve_rows_kernel<56>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
+        default: launch_pdl(chol_solve_rows_kernel<64>, dim3(gs), dim3(64), 0, s, Lm, n, M, rows, U, flag); break;
     }
     const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-    jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
-    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, n, M, rows, U, flag);
+    launch_pdl(jacobi_kernel, dim3(1), dim3(64), 0, s, H, n, V, gain, flag);
+    launch_pdl(jacobi_apply_rows_kernel, dim3(gb), dim3(128), 0, s, V, gain, n, M, rows, U, flag);
 }
 
 void launch_normalize(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
-    normalize_kernel<<<1, 256, 0, s>>>(U, rows, C, lambda);
+    launch_pdl(normalize_kernel, dim3(1), dim3(256), 0, s, U, rows, C, lambda);
 }
 
 void launch_fit(const double* U, const double* Mlast, long long rows, int C, const double* lambda, const double* Hlast,
                 const double* normx, double* out, cudaStream_t s) {
-    fit_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, normx, out);
+    launch_pdl(fit_kernel, dim3(1), dim3(256), 0, s, U, Mlast, rows, C, lambda, Hlast, normx, out);
 }
 
 void launch_tensor_norm(const double* x, long long n, double* part, int nparts, double* out, cudaStream_t s) {
-    sumsq_partial_kernel<<<nparts, 512, 0, s>>>(x, n, part);
-    sumsq_final_kernel<<<1, 32, 0, s>>>(part, nparts, out);
+    launch_pdl(sumsq_partial_kernel, dim3(nparts), dim3(512), 0, s, x, n, part);
+    launch_pdl(sumsq_final_kernel, dim3(1), dim3(32), 0, s, part, nparts, out);
 }
 
 void launch_gram(const double* U, long long rows, int C, double* G, cudaStream_t s) {
-    gram_warp_kernel<<<C * (C + 1) / 2, 32, 0, s>>>(U, rows, C, G, nullptr);
+    launch_pdl(gram_warp_kernel, dim3(C * (C + 1) / 2), dim3(32), 0, s, U, rows, C, G, nullptr);
 }
 
 void launch_hadamard_grams(const double* grams, int nmodes, int C, int skip, double* H, cudaStream_t s) {
-    hadamard_grams_kernel<<<(C * C + 127) / 128, 128, 0, s>>>(grams, nmodes, C, skip, H);
+    launch_pdl(hadamard_grams_kernel, dim3((C * C + 127) / 128), dim3(128), 0, s, grams, nmodes, C, skip, H);
 }
 
 void launch_col_sumsq(const double* U, long long rows, int C, double* sumsq, cudaStream_t s) {
-    normalize_cols_kernel<<<C, 256, 0, s>>>(const_cast<double*>(U), rows, C, nullptr, nullptr, sumsq, nullptr);
+    launch_pdl(normalize_cols_kernel, dim3(C), dim3(256), 0, s, const_cast<double*>(U), rows, C, nullptr, nullptr, sumsq, nullptr);
 }
 
 void launch_normalize_cols_by(double* U, long long rows, int C, const double* sumsq, double* lambda, cudaStream_t s) {
-    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr, nullptr, sumsq);
+    launch_pdl(normalize_cols_kernel, dim3(C), dim3(256), 0, s, U, rows, C, lambda, nullptr, nullptr, sumsq);
 }
 
 void launch_normalize_cols(double* U, long long rows, int C, double* lambda, cudaStream_t s) {
-    normalize_cols_kernel<<<C, 256, 0, s>>>(U, rows, C, lambda, nullptr);
+    launch_pdl(normalize_cols_kernel, dim3(C), dim3(256), 0, s, U, rows, C, lambda, nullptr, nullptr, nullptr);
 }
 
 void launch_solve_psd_inverse(const double* H, int n, const double* M, long long rows, double* U, double* scratch,
@@ -1205,14 +1264,14 @@ void launch_solve_psd_inverse(const double* H, int n, const double* M, long long
         cudaFuncSetAttribute(cholesky_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
     });
     if (n <= 32)
-        cholesky_inverse_rl_kernel<<<1, 32, 0, s>>>(H, n, Hinv, flag);
+        launch_pdl(cholesky_inverse_rl_kernel, dim3(1), dim3(32), 0, s, H, n, Hinv, flag);
     else
-        cholesky_inverse_kernel<<<1, 32, sm2, s>>>(H, n, Hinv, flag);
+        launch_pdl(cholesky_inverse_kernel, dim3(1), dim3(32), sm2, s, H, n, Hinv, flag);
     const long long tot = rows * n;
-    apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, n * n * 8, s>>>(Hinv, n, M, rows, U, flag);
-    jacobi_kernel<<<1, 64, 0, s>>>(H, n, V, gain, flag);
+    launch_pdl(apply_inverse_kernel, dim3(static_cast<unsigned>((tot + 255) / 256)), dim3(256), n * n * 8, s, Hinv, n, M, rows, U, flag);
+    launch_pdl(jacobi_kernel, dim3(1), dim3(64), 0, s, H, n, V, gain, flag);
     const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-    jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, n, M, rows, U, flag);
+    launch_pdl(jacobi_apply_rows_kernel, dim3(gb), dim3(128), 0, s, V, gain, n, M, rows, U, flag);
 }
 
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
@@ -1227,15 +1286,15 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         double* gain = V + 64 * 64;
         static const bool chol = std::getenv("DMTK_GPU_ALS_CHOL_INVERSE") != nullptr;
         if (chol)
-            als_solve_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
+            launch_pdl(als_solve_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
         else
-            als_solve_gj_kernel<<<1, 256, 0, s>>>(grams, nmodes, skip, C, H, Hinv, flag);
+            launch_pdl(als_solve_gj_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
         const long long tot = rows * C;
-        apply_inverse_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, C * C * 8, s>>>(Hinv, C, M, rows, U,
+        launch_pdl(apply_inverse_kernel, dim3(static_cast<unsigned>((tot + 255) / 256)), dim3(256), C * C * 8, s, Hinv, C, M, rows, U,
                                                                                             flag);
-        jacobi_kernel<<<1, 64, 0, s>>>(H, C, V, gain, flag);
+        launch_pdl(jacobi_kernel, dim3(1), dim3(64), 0, s, H, C, V, gain, flag);
         const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-        jacobi_apply_rows_kernel<<<gb, 128, 0, s>>>(V, gain, C, M, rows, U, flag);
+        launch_pdl(jacobi_apply_rows_kernel, dim3(gb), dim3(128), 0, s, V, gain, C, M, rows, U, flag);
         if (solve_only) return 4;
         launch_normalize_cols(U, rows, C, lambda, s);
         launch_gram(U, rows, C, Gn, s);
@@ -1254,18 +1313,18 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
 
 void launch_fit_cached(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                        const double* Hlast, const double* Glast, const double* normx, double* out, cudaStream_t s) {
-    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, Hlast, Glast, normx, out, nullptr, nullptr);
+    launch_pdl(fit_cached_kernel, dim3(1), dim3(256), 0, s, U, Mlast, rows, C, lambda, Hlast, Glast, normx, out, nullptr, nullptr);
 }
 
 void launch_fit_inner(const double* U, const double* Mlast, long long rows, int C, const double* lambda,
                       double* inner_out, cudaStream_t s) {
-    fit_cached_kernel<<<1, 256, 0, s>>>(U, Mlast, rows, C, lambda, nullptr, nullptr, nullptr, nullptr, nullptr,
+    launch_pdl(fit_cached_kernel, dim3(1), dim3(256), 0, s, U, Mlast, rows, C, lambda, nullptr, nullptr, nullptr, nullptr, nullptr,
                                         inner_out);
 }
 
 void launch_fit_from_inner(const double* lambda, int C, const double* Hlast, const double* Glast,
                            const double* normx, const double* inner, double* out, cudaStream_t s) {
-    fit_cached_kernel<<<1, 256, 0, s>>>(nullptr, nullptr, 0, C, lambda, Hlast, Glast, normx, out, inner, nullptr);
+    launch_pdl(fit_cached_kernel, dim3(1), dim3(256), 0, s, nullptr, nullptr, 0, C, lambda, Hlast, Glast, normx, out, inner, nullptr);
 }
 
 void launch_dmma_peak(double* out, int blocks, int iters, cudaStream_t s) {
