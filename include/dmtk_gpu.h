@@ -231,6 +231,15 @@ int dmtk_gpu_als_iterate(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, int 
  * symmetric slab (dmtk_gpu_tensor_pack_sym01 of this rank's slab) runs its
  * pair-index tree with Q all-reduced.
  *
+ * Exchanges (csrc/xrank.cu): by default every rank maps every
+ * other rank's receive buffer over NVLink (CUDA IPC handles exchanged with
+ * one NCCL all-gather at dmtk_gpu_comm_init) and each exchange is ONE kernel:
+ * for a mode's partials it is the MTTKRP's own slot reduction, which pushes
+ * this rank's rows into every peer and sums all ranks' rows in rank order --
+ * no separate ncclAllReduce, and the factors are bitwise identical on every
+ * rank. DMTK_GPU_XRANK=0 (read at communicator creation), or a failed peer
+ * mapping on any rank, keeps NCCL all-reduces.
+ *
  * dmtk_gpu_comm_unique_id: 128-byte NCCL id, made on one rank and broadcast
  * by the caller (e.g. torch.distributed) to all ranks, which then call
  * dmtk_gpu_comm_init with their rank and device. */
@@ -241,11 +250,35 @@ int dmtk_gpu_comm_free(dmtk_gpu_comm comm);
 /* Loopback communicators (tests of the sharded path without a second GPU):
  * `world` (1..16) virtual ranks on one device, comms_out[k] = rank k. Each
  * rank's dmtk_gpu_cp_als_sharded must run concurrently in its own host thread
- * (the all-reduces are host barriers plus stream events; ranks get separate
- * contexts and streams). Same exchanges, same code path as the NCCL
- * communicator except that the sweeps run eagerly (no CUDA graphs). Free
- * every handle with dmtk_gpu_comm_free. */
+ * (ranks get separate contexts and streams). Same exchanges, same code path
+ * and the same exchange kernel as the NCCL communicator, except that the
+ * sweeps run eagerly (no CUDA graphs) and each exchange runs the P ranks as
+ * ONE cooperative launch over the ranks' buffers on the device (rank 0's
+ * thread launches it once every rank has published its side: a host barrier
+ * plus stream events), never as separate launches waiting on one another.
+ * With DMTK_GPU_XRANK=0 the exchanges are stream-event all-reduces instead.
+ * Free every handle with dmtk_gpu_comm_free. */
 int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out);
+/* MTTKRP of a last-mode slab over the communicator: `slab` is
+ * this rank's slab, device_factors the full factors of modes 0..N-2 and this
+ * rank's rows of U_{N-1}. For mode n < N-1 device_out receives the full
+ * I_n x C result, summed over the ranks -- with the peer exchange that sum is
+ * the MTTKRP's own slot reduction (one kernel, rank order, the same bits on
+ * every rank), else an NCCL all-reduce follows; for the last mode it receives
+ * this rank's rows. Enqueued on `stream` (NULL: the legacy default stream);
+ * every rank calls it for the same modes in the same order (loopback ranks
+ * concurrently). */
+int dmtk_gpu_mttkrp_sharded(dmtk_gpu_comm comm, dmtk_gpu_tensor slab, const double* const* device_factors,
+                            int64_t rank, int64_t mode, int algo, int order, double* device_out, void* stream);
+/* rank, world, and fused = 1 when the exchanges run over peer memory
+ * (xrank), 0 for NCCL / event all-reduces. */
+int dmtk_gpu_comm_info(dmtk_gpu_comm comm, int* rank, int* world, int* fused);
+/* In-place sum over the communicator's ranks of n doubles in device memory,
+ * on `stream` (NULL: the library's stream; the call returns once the exchange
+ * is enqueued). With the peer exchange the sum is taken in rank order, so
+ * every rank gets the same bits; otherwise ncclAllReduce. Every rank calls it
+ * with the same n (loopback ranks concurrently, one host thread each). */
+int dmtk_gpu_comm_allreduce(dmtk_gpu_comm comm, double* device_buf, int64_t n, void* stream);
 int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t last_extent, int64_t last_lo,
                             const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out, double* fits_out,
                             double* iter_seconds_out, double* mode_seconds_out, int* n_iters, int* zero_tensor,
@@ -268,6 +301,12 @@ int dmtk_gpu_fp64_peak_sustained(int device, double seconds, double* tflops);
 /* Number of kernels this library has launched since load (for the
  * benchmark's gpu_launches claim). */
 int64_t dmtk_gpu_launch_count(void);
+
+/* Developer timeline of the last streaming MTTKRP launch on `device` when
+ * the process runs with DMTK_GPU_TRACE=1: 16 %globaltimer stamps (ns) per
+ * CTA, 0 = not reached; see TraceEv in csrc/mttkrp_plan.h. Not part of the
+ * reference interface. */
+int dmtk_gpu_debug_trace(int device, uint64_t* host_out, int max_ctas, int* n_ctas);
 
 #ifdef __cplusplus
 }

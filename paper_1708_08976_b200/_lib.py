@@ -75,11 +75,16 @@ _SIGS = {
     "dmtk_gpu_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dmtk_gpu_comm_free": (C.c_int, [C.c_void_p]),
     "dmtk_gpu_comm_loopback": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dmtk_gpu_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "dmtk_gpu_comm_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "dmtk_gpu_mttkrp_sharded": (C.c_int, [C.c_void_p, T, C.POINTER(C.c_void_p), C.c_int64, C.c_int64, C.c_int,
+                                          C.c_int, C.c_void_p, C.c_void_p]),
     "dmtk_gpu_cp_als_sharded": (C.c_int, [T, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(AlsConfig), dp, dp, dp, dp,
                                           dp, C.POINTER(C.c_int), C.POINTER(C.c_int), dp]),
     "dmtk_gpu_fp64_peak": (C.c_int, [C.c_int, dp]),
     "dmtk_gpu_fp64_peak_sustained": (C.c_int, [C.c_int, C.c_double, dp]),
     "dmtk_gpu_launch_count": (C.c_int64, []),
+    "dmtk_gpu_debug_trace": (C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -25,10 +25,17 @@ struct KrpGen {
     long long stride[kMaxFactors];
 };
 
+// 64-bit division, out of line: the software sequence is ~70 instructions,
+// and inlined at every index computation it made the streaming kernels
+// 14-24 K instructions long -- their one-shot code (prologue, builder set-up,
+// epilogue) then ran from instruction-cache misses, tens of microseconds per
+// launch once L2 had been flushed. The common (32-bit) paths stay inline.
+static __device__ __noinline__ long long div64_slow(long long a, long long b) { return a / b; }
+
 // a / b for non-negative operands, 32-bit when both fit.
 __device__ __forceinline__ long long div_nn(long long a, long long b) {
     if (a < 0x7fffffffLL && b < 0x7fffffffLL) return static_cast<unsigned>(a) / static_cast<unsigned>(b);
-    return a / b;
+    return div64_slow(a, b);
 }
 
 // Digit of factor f for a compound index (32-bit division when it fits).
@@ -37,7 +44,8 @@ __device__ __forceinline__ long long krp_digit(const KrpGen& g, int f, long long
         const unsigned q = static_cast<unsigned>(idx) / static_cast<unsigned>(g.stride[f]);
         return q % static_cast<unsigned>(g.ext[f]);
     }
-    return (idx / g.stride[f]) % g.ext[f];
+    const long long q = div64_slow(idx, g.stride[f]);
+    return q - div64_slow(q, g.ext[f]) * g.ext[f];
 }
 
 __device__ __forceinline__ double krp_value(const KrpGen& g, long long idx, int c) {

@@ -137,7 +137,8 @@ struct Context {
     cudaEvent_t ev[8] = {};
     std::recursive_mutex mu;
     DevBuf ones, ws, fac, out, scratch, scratch2, krp_scratch, htab, reorder, als_small, norm_parts, mttv, u0pad,
-        chunk_fac, chunk_out;
+        chunk_fac, chunk_out, trace;
+    int trace_ctas = 0;
     int* flag = nullptr;
     Context() = default;
 };
@@ -234,6 +235,9 @@ struct dmtk_gpu_tensor_s {
     double full_norm = 0.0;
     const double* d = nullptr;
     bool owned = false;
+    // the buffer is followed by kSlack zero doubles (library allocations): the
+    // 3-D TMA boxes of M-major views may read a last partial 16-row block
+    bool slack = false;
     std::mutex mu;
     // tensor maps (they hold the base address) are cached per tensor; plans
     // and CSR slot maps per shape (plans_of / csrs_of)
@@ -251,6 +255,32 @@ struct dmtk_gpu_tensor_s {
         }
     }
 };
+
+// The fused slot reduction of the streaming MTTKRP that produces `out`
+// (enqueue_planned), armed by the sharded CP-ALS for the modes whose I_n x C
+// partials are summed over the ranks (xrank_exchange, below).
+struct Shard;
+struct XrankTarget {
+    const Shard* sh;
+    double* out;
+    long long rows;
+    bool fired;
+};
+static thread_local XrankTarget* g_xtarget = nullptr;
+extern "C" {  // (defined in the extern "C" block below)
+static bool xrank_fits(const Shard* sh, long long rows, int C);
+static void xrank_exchange(const Shard* sh, const dmtkg::XrankLocal& loc, long long rows, int C, cudaStream_t s);
+}
+
+// Library-owned tensor buffers: n doubles followed by kSlack zeros
+// (stream-ordered pool allocation; see dmtk_gpu_tensor_s::slack).
+constexpr long long kSlack = 32;
+static cudaError_t tensor_malloc(double** p, long long n, cudaStream_t s) {
+    const long long m = std::max<long long>(n, 1);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), static_cast<size_t>(m + kSlack) * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(*p + m, 0, static_cast<size_t>(kSlack) * sizeof(double), s);
+}
 
 namespace dmtkg {
 
@@ -693,7 +723,20 @@ static CUtensorMap make_map(const double* base, const ModePlan& mp) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     CUresult r;
-    if (mp.kind == kTcM) {
+    if (mp.kind == kTcM && mp.tc.m3) {
+        // (16 m, j, m / 16): the last partial block reads up to 15 values past
+        // its column (rows of the next column, or the buffer's zero slack after
+        // the last one) -- padding rows of the tile, never used
+        const long long mrows = mp.L * mp.I;
+        const cuuint64_t gdim[3] = {16, static_cast<cuuint64_t>(mp.R), static_cast<cuuint64_t>((mrows + 15) / 16)};
+        const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(mrows * 8), 128};
+        const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(mp.tc.BK), static_cast<cuuint32_t>(mp.tc.TR / 16)};
+        const cuuint32_t es[3] = {1, 1, 1};
+        const auto promo = (mrows * 8) % 256 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), gdim, gstride, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else if (mp.kind == kTcM) {
         const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(mp.L * mp.I), static_cast<cuuint64_t>(mp.R)};
         const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(mp.L * mp.I * 8)};
         const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(mp.tc.BK)};
@@ -801,10 +844,28 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
             }
         }
         if (const char* dbg = std::getenv("DMTK_GPU_DEBUG")) mp.tc.debug = std::atoi(dbg);
+        // DMTK_GPU_TRACE=1: per-CTA timeline stamps of the last launch (dmtk_gpu_debug_trace)
+        static const bool trace_on = std::getenv("DMTK_GPU_TRACE") != nullptr;
+        mp.tc.trace = nullptr;
+        if (trace_on) {
+            ctx.trace.ensure(static_cast<size_t>(mp.grid) * kTraceSlots);
+            CK(cudaMemsetAsync(ctx.trace.p, 0, static_cast<size_t>(mp.grid) * kTraceSlots * 8, s));
+            mp.tc.trace = reinterpret_cast<unsigned long long*>(ctx.trace.p);
+            ctx.trace_ctas = mp.grid;
+        }
         mp.tc.X = X;
         mp.tc.x_wait = X != t.d;  // a scratch copy (baseline matricisation) may still be in flight
         static const bool force_ldgsts = std::getenv("DMTK_GPU_FORCE_LDGSTS") != nullptr;
         if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || force_ldgsts) mp.tc.ldgsts = 1;
+        // M-major stages as one 3-D TMA box per row group (TR / 16 fewer TMA
+        // instructions: the producer's issue rate bounded M-major streaming at
+        // ~1 us per 32 KB stage) when the last partial 16-row block may read
+        // past its column: whole 16-row blocks, or a buffer with zero slack
+        static const bool no_m3 = std::getenv("DMTK_GPU_NO_M3") != nullptr;
+        mp.tc.m3 = (mp.kind == kTcM && !mp.tc.ldgsts && !no_m3 && X == t.d &&
+                    ((mp.L * mp.I) % 16 == 0 || t.slack) && mp.tc.TR / 16 <= 256)
+                       ? 1
+                       : 0;
         static const bool plan_log = std::getenv("DMTK_GPU_PLAN_LOG") != nullptr;
         if (plan_log)
             std::fprintf(stderr,
@@ -818,7 +879,8 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         if (mp.tc.ldgsts) {
             std::memset(&map, 0, sizeof(map));
         } else if (X == t.d) {  // the tensor itself: one encode per view
-            const std::array<long long, 7> mkey{mp.kind, mp.L, mp.I, mp.R, mp.tc.BK, mp.tc.BI, mp.tc.BJ};
+            const std::array<long long, 7> mkey{mp.kind + 16 * mp.tc.m3 + 32 * mp.tc.TR, mp.L, mp.I, mp.R, mp.tc.BK,
+                                                mp.tc.BI, mp.tc.BJ};
             auto mit = t.maps.find(mkey);
             if (mit == t.maps.end()) mit = t.maps.emplace(mkey, make_map(X, mp)).first;
             map = mit->second;
@@ -830,8 +892,15 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         check_launch("mttkrp_tc");
     }
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[3], s));
-    launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s, csr.nslots);
-    check_launch("slot_reduce");
+    XrankTarget* xt = g_xtarget;
+    if (xt && !xt->fired && xt->out == dout && xt->rows == mp.out_rows && xrank_fits(xt->sh, mp.out_rows, C)) {
+        // sharded CP-ALS: the slot reduction and the sum over the ranks in one kernel
+        xrank_exchange(xt->sh, XrankLocal{ctx.ws.p, csr.rowptr.p, csr.slots.p, dout, nullptr}, mp.out_rows, C, s);
+        xt->fired = true;
+    } else {
+        launch_slot_reduce(ctx.ws.p, csr.rowptr.p, csr.slots.p, mp.out_rows, C, dout, s, csr.nslots);
+        check_launch("slot_reduce");
+    }
     if (ph && ph->record) CK(cudaEventRecord(ctx.ev[4], s));
 }
 
@@ -850,8 +919,7 @@ static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
     if (odd) pd[0] += 1;
     const long long pt = prod(pd, 0, static_cast<int>(pd.size()));
     double* p = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(pt) * sizeof(double), ctx.stream) !=
-        cudaSuccess) {
+    if (tensor_malloc(&p, pt, ctx.stream) != cudaSuccess) {
         cudaGetLastError();
         t.repack_failed = true;
         return;
@@ -865,6 +933,7 @@ static void ensure_layout(dmtk_gpu_tensor_s& t, Context& ctx, cudaStream_t s) {
     CK(cudaStreamSynchronize(ctx.stream));
     t.user = t.d;
     t.d = p;
+    t.slack = true;
     t.pdims = pd;
     t.ptotal = pt;
     t.maps.clear();  // plans and slot maps are keyed by the new layout
@@ -1589,11 +1658,10 @@ int dmtk_gpu_tensor_upload(int device, int ndim, const int64_t* dims, const doub
         double* p = nullptr;
         // stream-ordered pool allocation: repeated upload/free cycles reuse the
         // pool instead of paying cudaMalloc/cudaFree for every 8 GB tensor
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(std::max<long long>(t->ptotal, 1)) *
-                                                             sizeof(double),
-                           ctx.stream));
+        CK(tensor_malloc(&p, t->ptotal, ctx.stream));
         t->d = p;
         t->owned = true;
+        t->slack = true;
         if (t->pdims == t->dims) {
             CK(cudaMemcpyAsync(p, host, static_cast<size_t>(t->total) * sizeof(double), cudaMemcpyHostToDevice,
                                ctx.stream));
@@ -1629,11 +1697,10 @@ int dmtk_gpu_tensor_generate(int device, int ndim, const int64_t* dims, uint64_t
         if (ndim > 0 && d[0] % 2 != 0 && t->total > 0) t->pdims[0] = d[0] + 1;  // same layout as an upload
         t->ptotal = prod(t->pdims, 0, ndim);
         double* p = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(std::max<long long>(t->ptotal, 1)) *
-                                                             sizeof(double),
-                           ctx.stream));
+        CK(tensor_malloc(&p, t->ptotal, ctx.stream));
         t->d = p;
         t->owned = true;
+        t->slack = true;
         if (t->pdims != t->dims) CK(cudaMemsetAsync(p, 0, static_cast<size_t>(t->ptotal) * sizeof(double), ctx.stream));
         if (t->total > 0) {
             if (dist == 1) {
@@ -1762,9 +1829,10 @@ int dmtk_gpu_tensor_load(int device, const char* path, dmtk_gpu_tensor* out) {
         if (d[0] % 2 != 0) t->pdims[0] = d[0] + 1;  // same padded layout as dmtk_gpu_tensor_upload
         t->ptotal = prod(t->pdims, 0, static_cast<int>(n));
         double* p = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(t->ptotal) * sizeof(double), ctx.stream));
+        CK(tensor_malloc(&p, t->ptotal, ctx.stream));
         t->d = p;
         t->owned = true;
+        t->slack = true;
         // chunks of whole mode-0 runs (the padded copy is pitched per run)
         const long long run = d[0];
         const long long runs = t->total / run;
@@ -1870,9 +1938,10 @@ int dmtk_gpu_tensor_pack_sym01(dmtk_gpu_tensor t, dmtk_gpu_tensor* out) {
         p->sym01 = true;
         p->full_norm = norm;
         double* buf = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), static_cast<size_t>(p->ptotal) * sizeof(double), ctx.stream));
+        CK(tensor_malloc(&buf, p->ptotal, ctx.stream));
         p->d = buf;
         p->owned = true;
+        p->slack = true;
         launch_sym01_pack(t->d, I, pd0, R, Pp, buf, ctx.stream);
         check_launch("sym01_pack");
         CK(cudaStreamSynchronize(ctx.stream));
@@ -1906,9 +1975,10 @@ int dmtk_gpu_tensor_slab(dmtk_gpu_tensor t, int64_t lo, int64_t hi, dmtk_gpu_ten
         }
         p->ptotal = prod(p->pdims, 0, N);
         double* buf = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), static_cast<size_t>(p->ptotal) * sizeof(double), ctx.stream));
+        CK(tensor_malloc(&buf, p->ptotal, ctx.stream));
         p->d = buf;
         p->owned = true;
+        p->slack = true;
         CK(cudaMemcpyAsync(buf, t->d + first, static_cast<size_t>(count) * sizeof(double), cudaMemcpyDeviceToDevice,
                            ctx.stream));
         if (p->ptotal > count)
@@ -2004,37 +2074,15 @@ int dmtk_gpu_mttkrp(dmtk_gpu_tensor t, int nfactors, const double* const* factor
     });
 }
 
+static void mttkrp_device_impl(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode,
+                               int algo, int order, double* device_out, void* stream, dmtk_gpu_comm comm);
+
 int dmtk_gpu_mttkrp_device(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode, int algo,
                            int order, double* device_out, void* stream) {
-    return guarded([&] {
-        if (!t) fail(DMTK_GPU_EINVAL, "mttkrp: null tensor");
-        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
-        const int N = static_cast<int>(t->dims.size());
-        if (mode < 0 || mode >= N)
-            fail(DMTK_GPU_ERANGE, "mttkrp: mode " + std::to_string(mode) + " outside [0, " + std::to_string(N) + ")");
-        if (rank < 1) fail(DMTK_GPU_EINVAL, "mttkrp: rank must be >= 1");
-        const int ralgo = resolve_algo(algo, static_cast<int>(mode), N);
-        if (ralgo == DMTK_GPU_TWO_STEP && (mode == 0 || mode == N - 1))
-            fail(DMTK_GPU_EINVAL, "mttkrp_two_step: mode " + std::to_string(mode) +
-                                      " is a boundary mode with a degenerate partial KRP; use one_step instead");
-        Context& ctx = context(t->device);
-        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
-        CK(cudaSetDevice(t->device));  // plans and slot maps are cached per device
-        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
-        ensure_layout(*t, ctx, s);
-        std::vector<const double*> f(device_factors, device_factors + N);
-        if (t->pdims[0] != t->dims[0]) {  // padded tensor: first factor with a zero row
-            const size_t rowsz = static_cast<size_t>(rank) * sizeof(double);
-            ctx.u0pad.ensure(static_cast<size_t>(t->pdims[0] * rank));
-            CK(cudaMemcpyAsync(ctx.u0pad.p, f[0], static_cast<size_t>(t->dims[0]) * rowsz, cudaMemcpyDeviceToDevice, s));
-            CK(cudaMemsetAsync(ctx.u0pad.p + t->dims[0] * rank, 0, static_cast<size_t>(t->pdims[0] - t->dims[0]) * rowsz,
-                               s));
-            f[0] = ctx.u0pad.p;
-        }
-        mttkrp_enqueue(*t, ctx, f.data(), static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out, s,
-                       nullptr);
-    });
+    return guarded([&] { mttkrp_device_impl(t, device_factors, rank, mode, algo, order, device_out, stream, nullptr); });
 }
+
+
 
 int dmtk_gpu_krp_device(int z, const double* const* device_inputs, const int64_t* rows, int64_t cols, double* device_out,
                         double* device_scratch, void* stream) {
@@ -2210,6 +2258,7 @@ struct NcclApi {
     ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
@@ -2226,8 +2275,11 @@ static NcclApi& nccl() {
         a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.h, "ncclCommInitRank"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.h, "ncclAllReduce"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.h, "ncclCommDestroy"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(a.h, "ncclAllGather"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.h, "ncclGetErrorString"));
-        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.comm_destroy || !a.error_string) a.h = nullptr;
+        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.all_gather || !a.comm_destroy ||
+            !a.error_string)
+            a.h = nullptr;
         return a;
     }();
     if (!api.h) fail(DMTK_GPU_ERUNTIME, "NCCL (libnccl.so.2) is not available");
@@ -2248,6 +2300,42 @@ static void nccl_check(ncclResult_t r, const char* what) {
 // events, so they cannot deadlock however the device schedules them. The
 // production NCCL path is unchanged; the loopback runs the same sharded CP-ALS
 // code (eagerly: no CUDA graphs, whose replays would race the host barrier).
+// Peer-memory exchange state of one rank (xrank.cu): its own receive
+// buffer [2][P][cap], flag array [P][kXNblkCap] and block epoch counters,
+// plus every rank's receive buffer and flags as this process sees them
+// (CUDA IPC peer mappings over NVLink, or one device's buffers for the
+// loopback group).
+constexpr int kXNblkCap = 64;
+struct XrankGroup {
+    int P = 1, rank = 0;
+    long long cap = 0;
+    int nblk = 1;                  // blocks per launch (identical on every rank)
+    bool emulated = false;         // loopback: the ranks run as one launch
+    void* own = nullptr;           // this rank's allocation: recv | flags | ctr
+    double* recv[kLoopMax] = {};
+    unsigned long long* flags[kLoopMax] = {};
+    unsigned long long* ctr = nullptr;
+    std::vector<void*> opened;     // IPC mappings to close
+    static size_t bytes(int P, long long cap) {
+        return static_cast<size_t>(2 * P * cap) * 8 + static_cast<size_t>(P + 1) * kXNblkCap * 8;
+    }
+    void carve(void* base, int k) {  // rank k's recv and flags inside its allocation
+        recv[k] = static_cast<double*>(base);
+        flags[k] = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(base) +
+                                                         static_cast<size_t>(2 * P * cap) * 8);
+    }
+    ~XrankGroup() {
+        for (void* q : opened) cudaIpcCloseMemHandle(q);
+        if (own) cudaFree(own);
+        cudaGetLastError();
+    }
+};
+
+static long long xrank_cap(long long dflt) {
+    const char* e = std::getenv("DMTK_GPU_XRANK_CAP");  // doubles per sender row
+    return e && std::atoll(e) > 0 ? std::atoll(e) : dflt;
+}
+
 struct LoopGroup {
     int P = 0, device = 0;
     std::mutex mu;
@@ -2257,6 +2345,10 @@ struct LoopGroup {
     std::vector<double*> bufs;
     std::vector<cudaEvent_t> ready, done;
     std::vector<DevBuf> sums;
+    // fused exchange (xrank): one group state per virtual rank and the
+    // launch being assembled (each rank publishes its side)
+    std::vector<std::unique_ptr<XrankGroup>> xr;
+    XrankArgs pub{};
     int refs = 0;
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
@@ -2277,10 +2369,79 @@ struct Shard {
     int rank;               // this rank in the group
     long long last_extent;  // global extent of the last mode
     long long last_lo;      // this rank's first last-mode row
+    XrankGroup* xr;         // peer-memory exchange (fused reductions), or null (NCCL all-reduce)
 };
 
-static void shard_allreduce(const Shard* sh, double* p, long long n, cudaStream_t s) {
+// One fused exchange: every rank's local rows x C values (a buffer, or the
+// slot sums of its streaming MTTKRP) summed over the ranks in rank order
+// into each rank's out. Loopback: rank 0 launches all P virtual ranks as one
+// cooperative kernel once every rank has published its side (host barrier)
+// and its inputs are ready (events); the others wait for that launch.
+static void xrank_exchange(const Shard* sh, const XrankLocal& loc, long long rows, int C, cudaStream_t s) {
+    XrankGroup& x = *sh->xr;
+    XrankLocal me = loc;
+    me.ctr = x.ctr;
+    if (!x.emulated) {
+        XrankArgs a{};
+        a.P = x.P;
+        a.rank0 = x.rank;
+        a.C = C;
+        a.rows = rows;
+        a.cap = x.cap;
+        a.nblk_cap = kXNblkCap;
+        for (int k = 0; k < x.P; ++k) {
+            a.recv[k] = x.recv[k];
+            a.flags[k] = x.flags[k];
+        }
+        a.me[0] = me;
+        CK(launch_xrank_reduce(a, x.nblk, 1, s));
+        check_launch("xrank_reduce");
+        return;
+    }
+    LoopGroup& g = *sh->loop;
+    const int r = sh->rank;
+    CK(cudaEventRecord(g.ready[r], s));
+    g.pub.me[r] = me;
+    g.barrier();  // every rank's side and ready event are published
+    if (r == 0) {
+        XrankArgs a = g.pub;
+        a.P = x.P;
+        a.rank0 = 0;
+        a.C = C;
+        a.rows = rows;
+        a.cap = x.cap;
+        a.nblk_cap = kXNblkCap;
+        for (int k = 0; k < x.P; ++k) {
+            a.recv[k] = x.recv[k];
+            a.flags[k] = x.flags[k];
+            if (k != 0) CK(cudaStreamWaitEvent(s, g.ready[k], 0));
+        }
+        CK(launch_xrank_reduce(a, x.nblk, x.P, s));
+        check_launch("xrank_reduce");
+        CK(cudaEventRecord(g.done[0], s));
+    }
+    g.barrier();  // the launch (and its done event) is enqueued
+    if (r != 0) CK(cudaStreamWaitEvent(s, g.done[0], 0));
+}
+
+
+static bool xrank_fits(const Shard* sh, long long rows, int C) {
+    return sh && sh->xr && rows * C <= sh->xr->cap && C <= kXNblkCap * 4;
+}
+
+static void shard_allreduce(const Shard* sh, double* p, long long n, cudaStream_t s, int C = 1) {
     if (!sh || n <= 0) return;
+    if (sh->xr) {  // peer-memory exchange, chunks of at most cap values (rows x C when it fits)
+        if (n <= sh->xr->cap && n % C == 0) {
+            xrank_exchange(sh, XrankLocal{p, nullptr, nullptr, p, nullptr}, n / C, C, s);
+        } else {
+            for (long long o = 0; o < n; o += sh->xr->cap) {
+                const long long m = std::min(sh->xr->cap, n - o);
+                xrank_exchange(sh, XrankLocal{p + o, nullptr, nullptr, p + o, nullptr}, m, 1, s);
+            }
+        }
+        return;
+    }
     if (!sh->loop) {
         nccl_check(nccl().all_reduce(p, p, static_cast<size_t>(n), ncclFloat64, ncclSum, sh->comm, s),
                    "ncclAllReduce");
@@ -2476,9 +2637,28 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             shard_allreduce(sh, Gn, static_cast<long long>(C) * C, s);
             fitM = Mn;
         };
+        // A partial summed over the shards: the producing MTTKRP's slot reduction
+        // does the exchange (xrank, one kernel) when it can, else an all-reduce
+        // of the same rows x C geometry follows
+        auto reduced_enqueue = [&](double* out, long long rows, const std::function<void()>& enqueue) {
+            XrankTarget xt{sh, out, rows, false};
+            if (xrank_fits(sh, rows, C)) g_xtarget = &xt;
+            try {
+                enqueue();
+            } catch (...) {
+                g_xtarget = nullptr;
+                throw;
+            }
+            g_xtarget = nullptr;
+            if (sh && !xt.fired) shard_allreduce(sh, out, rows * C, s, C);
+        };
         auto mode_step = [&](int n) {
-            mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
-            if (sh && n < N - 1) shard_allreduce(sh, M.p, t->dims[n] * C, s);  // the I_n x C partials
+            if (sh && n < N - 1)  // the I_n x C partials
+                reduced_enqueue(M.p, t->dims[n], [&] {
+                    mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
+                });
+            else
+                mttkrp_enqueue(*t, ctx, Uc.data(), C, n, cfg->algo, cfg->order, M.p, s, nullptr);
             if (sh && n == N - 1)
                 als_upd_sharded_last(n, M.p);
             else
@@ -2510,8 +2690,12 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             const ModePlan mp = plan_view(1, rowsL, rowsR, C, kTcM, 0, ctx.sms);
             const KrpGen bg = make_gen(t->pdims, hsplit, N, Uc.data(), C, ctx.ones.p);
             const KrpGen sg = make_gen(t->pdims, 0, 0, Uc.data(), C, ctx.ones.p);
-            enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
-            shard_allreduce(sh, Pbuf.p, rowsL * C, s);  // sharded: the left partial summed over the slabs
+            if (sh)  // sharded: the left partial summed over the slabs
+                reduced_enqueue(Pbuf.p, rowsL, [&] {
+                    enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
+                });
+            else
+                enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, (200 + hsplit) * 128, -1, Pbuf.p, s, nullptr);
         };
         auto pass_right = [&]() {
             const ModePlan mp = plan_view(rowsL, rowsR, 1, C, kTcKJ, 0, ctx.sms);
@@ -2542,7 +2726,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
             launch_multittv(Pbuf.p, C, A, dt, B, kl, kr, ctx.mttv.p, M.p, s);
             count_launch(1);
             check_launch("multittv");
-            if (sh && lo > 0 && k < N - 1) shard_allreduce(sh, M.p, dt * C, s);  // a right-half mode
+            if (sh && lo > 0 && k < N - 1) shard_allreduce(sh, M.p, dt * C, s, C);  // a right-half mode
             upd(k, M.p);
         };
         struct Step {
@@ -2569,8 +2753,12 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
                 const ModePlan mp = plan_view(1, sPp, sR, C, kTcM, 0, ctx.sms);
                 const KrpGen bg = make_gen(t->pdims, 1, Np, pk_ptrs.data(), C, ctx.ones.p);
                 const KrpGen sg = make_gen(t->pdims, 0, 0, pk_ptrs.data(), C, ctx.ones.p);
-                enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, 400 * 128, -1, Qb.p, s, nullptr);
-                shard_allreduce(sh, Qb.p, sPp * C, s);  // sharded: Q summed over the slabs
+                if (sh)  // sharded: Q summed over the slabs
+                    reduced_enqueue(Qb.p, sPp, [&] {
+                        enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, 400 * 128, -1, Qb.p, s, nullptr);
+                    });
+                else
+                    enqueue_planned(*t, ctx, mp, kTcM, bg, sg, t->d, C, 400 * 128, -1, Qb.p, s, nullptr);
             };
             auto sym_mode = [&](int k) {  // mode 0 (with U_1) or mode 1 (with the new U_0)
                 launch_sym01_mttv(Qb.p, sI, C, k == 0 ? Um[1] : Um[0], M.p, s);
@@ -2784,7 +2972,27 @@ struct dmtk_gpu_comm_s {
     ncclComm_t comm = nullptr;
     LoopGroup* loop = nullptr;
     int rank = 0, world = 1, device = 0;
+    XrankGroup* xr = nullptr;                 // the peer-memory exchange, or null (NCCL all-reduce)
+    std::unique_ptr<XrankGroup> xr_owned;     // (NCCL ranks own theirs; the loopback group owns its ranks')
 };
+
+static bool xrank_wanted() {
+    const char* e = std::getenv("DMTK_GPU_XRANK");  // 0: NCCL all-reduce / event all-reduce instead
+    return !(e && std::string(e) == "0");
+}
+
+// zeroed allocation holding recv | flags | ctr for P ranks of cap values
+static void* xrank_alloc(int P, long long cap) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, XrankGroup::bytes(P, cap)));
+    CK(cudaMemset(p, 0, XrankGroup::bytes(P, cap)));
+    CK(cudaDeviceSynchronize());  // zeroed before any peer (or non-blocking stream) touches it
+    return p;
+}
+static unsigned long long* xrank_ctr_of(void* base, int P, long long cap) {
+    return reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(base) + static_cast<size_t>(2 * P * cap) * 8 +
+                                                 static_cast<size_t>(P) * kXNblkCap * 8);
+}
 
 int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out) {
     return guarded([&] {
@@ -2804,6 +3012,26 @@ int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out) {
             CK(cudaEventCreateWithFlags(&g->ready[k], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&g->done[k], cudaEventDisableTiming));
         }
+        if (xrank_wanted()) {
+            // the fused exchange over one device's buffers: every virtual rank's
+            // receive buffer and flags, launched as one kernel for all ranks
+            const long long cap = xrank_cap(1LL << 18);
+            const int nblk = std::max(1, std::min(kXNblkCap, xrank_max_blocks() / world));
+            std::vector<void*> base(world);
+            for (int k = 0; k < world; ++k) base[k] = xrank_alloc(world, cap);
+            for (int k = 0; k < world; ++k) {
+                auto x = std::make_unique<XrankGroup>();
+                x->P = world;
+                x->rank = k;
+                x->cap = cap;
+                x->nblk = nblk;
+                x->emulated = true;
+                x->own = base[k];
+                for (int j = 0; j < world; ++j) x->carve(base[j], j);
+                x->ctr = xrank_ctr_of(base[k], world, cap);
+                g->xr.push_back(std::move(x));
+            }
+        }
         g->refs = world;
         for (int k = 0; k < world; ++k) {
             auto c = new dmtk_gpu_comm_s;
@@ -2811,6 +3039,7 @@ int dmtk_gpu_comm_loopback(int world, int device, dmtk_gpu_comm* comms_out) {
             c->rank = k;
             c->world = world;
             c->device = device;
+            if (!g->xr.empty()) c->xr = g->xr[k].get();
             comms_out[k] = c;
         }
     });
@@ -2838,6 +3067,61 @@ int dmtk_gpu_comm_init(const unsigned char* id128, int rank, int world, int devi
         c->rank = rank;
         c->world = world;
         c->device = device;
+        if (xrank_wanted() && world <= kLoopMax) {
+            // fused exchange over NVLink peer memory: each rank allocates its
+            // receive buffer and flags, the IPC handles go round with one NCCL
+            // all-gather, and every rank maps every peer's allocation. Any
+            // failure on any rank (checked with a min all-reduce) leaves every
+            // rank on the NCCL all-reduce.
+            Context& ctx = context(device);
+            const long long cap = xrank_cap(1LL << 20);
+            auto x = std::make_unique<XrankGroup>();
+            x->P = world;
+            x->rank = rank;
+            x->cap = cap;
+            x->nblk = std::min(kXNblkCap, xrank_max_blocks());
+            x->own = xrank_alloc(world, cap);
+            x->carve(x->own, rank);
+            x->ctr = xrank_ctr_of(x->own, world, cap);
+            cudaIpcMemHandle_t mine{};
+            double ok = 1.0;
+            if (world > 1 && cudaIpcGetMemHandle(&mine, x->own) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0.0;
+            }
+            DevBuf hb;
+            hb.ensure(static_cast<size_t>(world) * 8 + 8 + 1);  // 64-byte handles (8 doubles each) + the flag
+            std::vector<cudaIpcMemHandle_t> all(world);
+            if (world > 1) {
+                CK(cudaMemcpyAsync(hb.p + rank * 8, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx.stream));
+                nccl_check(nccl().all_gather(hb.p + rank * 8, hb.p, 64, ncclChar, c->comm, ctx.stream),
+                           "ncclAllGather");
+                CK(cudaMemcpyAsync(all.data(), hb.p, static_cast<size_t>(world) * 64, cudaMemcpyDeviceToHost,
+                                   ctx.stream));
+                CK(cudaStreamSynchronize(ctx.stream));
+                for (int k = 0; k < world && ok > 0.0; ++k) {
+                    if (k == rank) continue;
+                    void* q = nullptr;
+                    if (cudaIpcOpenMemHandle(&q, all[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                        cudaGetLastError();
+                        ok = 0.0;
+                        break;
+                    }
+                    x->opened.push_back(q);
+                    x->carve(q, k);
+                }
+                CK(cudaMemcpyAsync(hb.p + world * 8, &ok, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+                nccl_check(nccl().all_reduce(hb.p + world * 8, hb.p + world * 8, 1, ncclFloat64, ncclMin, c->comm,
+                                             ctx.stream),
+                           "ncclAllReduce");
+                CK(cudaMemcpyAsync(&ok, hb.p + world * 8, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+                CK(cudaStreamSynchronize(ctx.stream));
+            }
+            if (ok > 0.0) {
+                c->xr_owned = std::move(x);
+                c->xr = c->xr_owned.get();
+            }
+        }
         *out = c.release();
     });
 }
@@ -2845,6 +3129,11 @@ int dmtk_gpu_comm_init(const unsigned char* id128, int rank, int world, int devi
 int dmtk_gpu_comm_free(dmtk_gpu_comm c) {
     return guarded([&] {
         if (!c) return;
+        if (c->xr_owned) {
+            cudaSetDevice(c->device);
+            cudaDeviceSynchronize();
+            c->xr_owned.reset();
+        }
         if (c->comm) nccl().comm_destroy(c->comm);
         if (c->loop) {
             LoopGroup* g = c->loop;
@@ -2865,6 +3154,33 @@ int dmtk_gpu_comm_free(dmtk_gpu_comm c) {
     });
 }
 
+int dmtk_gpu_comm_info(dmtk_gpu_comm comm, int* rank, int* world, int* fused) {
+    return guarded([&] {
+        if (!comm || !rank || !world || !fused) fail(DMTK_GPU_EINVAL, "comm_info: null argument");
+        *rank = comm->rank;
+        *world = comm->world;
+        *fused = comm->xr ? 1 : 0;
+    });
+}
+
+int dmtk_gpu_comm_allreduce(dmtk_gpu_comm comm, double* device_buf, int64_t n, void* stream) {
+    return guarded([&] {
+        if (!comm) fail(DMTK_GPU_EINVAL, "comm_allreduce: null communicator");
+        if (n < 0 || (n > 0 && !device_buf)) fail(DMTK_GPU_EINVAL, "comm_allreduce: bad buffer");
+        struct SlotGuard {
+            int prev;
+            ~SlotGuard() { g_slot = prev; }
+        } guard{g_slot};
+        if (comm->loop) g_slot = 1 + comm->rank;  // the rank's own execution slot (context, stream)
+        Context& ctx = context(comm->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(comm->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx.stream;
+        const Shard sh{comm->comm, comm->loop, comm->rank, 0, 0, comm->xr};
+        shard_allreduce(&sh, device_buf, n, s);
+    });
+}
+
 int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t last_extent, int64_t last_lo,
                             const dmtk_gpu_als_config* cfg, double* factors_out, double* lambda_out, double* fits_out,
                             double* iter_seconds_out, double* mode_seconds_out, int* n_iters, int* zero_tensor,
@@ -2873,7 +3189,7 @@ int dmtk_gpu_cp_als_sharded(dmtk_gpu_tensor slab, dmtk_gpu_comm comm, int64_t la
         if (!comm) fail(DMTK_GPU_EINVAL, "cp_als_sharded: null communicator");
         if (slab && slab->device != comm->device)
             fail(DMTK_GPU_EINVAL, "cp_als_sharded: the slab and the communicator are on different devices");
-        const Shard sh{comm->comm, comm->loop, comm->rank, last_extent, last_lo};
+        const Shard sh{comm->comm, comm->loop, comm->rank, last_extent, last_lo, comm->xr};
         // a loopback rank runs in its own execution slot (context and caches)
         struct SlotGuard {
             int prev;
@@ -2993,4 +3309,83 @@ int dmtk_gpu_fp64_peak(int device, double* tflops) {
     });
 }
 
+int dmtk_gpu_mttkrp_sharded(dmtk_gpu_comm comm, dmtk_gpu_tensor slab, const double* const* device_factors,
+                            int64_t rank, int64_t mode, int algo, int order, double* device_out, void* stream) {
+    return guarded([&] {
+        if (!comm) fail(DMTK_GPU_EINVAL, "mttkrp_sharded: null communicator");
+        if (slab && slab->device != comm->device)
+            fail(DMTK_GPU_EINVAL, "mttkrp_sharded: the slab and the communicator are on different devices");
+        struct SlotGuard {
+            int prev;
+            ~SlotGuard() { g_slot = prev; }
+        } guard{g_slot};
+        if (comm->loop) g_slot = 1 + comm->rank;  // the loopback rank's own execution slot
+        mttkrp_device_impl(slab, device_factors, rank, mode, algo, order, device_out, stream, comm);
+    });
+}
+
+static void mttkrp_device_impl(dmtk_gpu_tensor t, const double* const* device_factors, int64_t rank, int64_t mode,
+                               int algo, int order, double* device_out, void* stream, dmtk_gpu_comm comm) {
+    {
+        if (!t) fail(DMTK_GPU_EINVAL, "mttkrp: null tensor");
+        if (t && t->sym01) fail(DMTK_GPU_EINVAL, "packed symmetric tensor: only cp_als and tensor_norm apply");
+        const int N = static_cast<int>(t->dims.size());
+        if (mode < 0 || mode >= N)
+            fail(DMTK_GPU_ERANGE, "mttkrp: mode " + std::to_string(mode) + " outside [0, " + std::to_string(N) + ")");
+        if (rank < 1) fail(DMTK_GPU_EINVAL, "mttkrp: rank must be >= 1");
+        const int ralgo = resolve_algo(algo, static_cast<int>(mode), N);
+        if (ralgo == DMTK_GPU_TWO_STEP && (mode == 0 || mode == N - 1))
+            fail(DMTK_GPU_EINVAL, "mttkrp_two_step: mode " + std::to_string(mode) +
+                                      " is a boundary mode with a degenerate partial KRP; use one_step instead");
+        Context& ctx = context(t->device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(t->device));  // plans and slot maps are cached per device
+        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+        ensure_layout(*t, ctx, s);
+        std::vector<const double*> f(device_factors, device_factors + N);
+        if (t->pdims[0] != t->dims[0]) {  // padded tensor: first factor with a zero row
+            const size_t rowsz = static_cast<size_t>(rank) * sizeof(double);
+            ctx.u0pad.ensure(static_cast<size_t>(t->pdims[0] * rank));
+            CK(cudaMemcpyAsync(ctx.u0pad.p, f[0], static_cast<size_t>(t->dims[0]) * rowsz, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemsetAsync(ctx.u0pad.p + t->dims[0] * rank, 0, static_cast<size_t>(t->pdims[0] - t->dims[0]) * rowsz,
+                               s));
+            f[0] = ctx.u0pad.p;
+        }
+        if (comm && mode < N - 1) {
+            // the I_n x C partial summed over the slabs: fused into the slot
+            // reduction when it can be, else an all-reduce of the same geometry
+            const Shard sh{comm->comm, comm->loop, comm->rank, 0, 0, comm->xr};
+            XrankTarget xt{&sh, device_out, t->dims[mode], false};
+            if (xrank_fits(&sh, t->dims[mode], static_cast<int>(rank))) g_xtarget = &xt;
+            try {
+                mttkrp_enqueue(*t, ctx, f.data(), static_cast<int>(rank), static_cast<int>(mode), algo, order,
+                               device_out, s, nullptr);
+            } catch (...) {
+                g_xtarget = nullptr;
+                throw;
+            }
+            g_xtarget = nullptr;
+            if (!xt.fired) shard_allreduce(&sh, device_out, t->dims[mode] * rank, s, static_cast<int>(rank));
+            return;
+        }
+        mttkrp_enqueue(*t, ctx, f.data(), static_cast<int>(rank), static_cast<int>(mode), algo, order, device_out, s,
+                       nullptr);
+    }
+}
+
 }  // extern "C"
+
+int dmtk_gpu_debug_trace(int device, uint64_t* host_out, int max_ctas, int* n_ctas) {
+    return guarded([&] {
+        if (!host_out || !n_ctas) fail(DMTK_GPU_EINVAL, "debug_trace: null argument");
+        Context& ctx = context(device);
+        std::lock_guard<std::recursive_mutex> lk(ctx.mu);
+        CK(cudaSetDevice(device));
+        const int n = std::min(ctx.trace_ctas, max_ctas);
+        *n_ctas = n;
+        if (n <= 0) return;
+        CK(cudaStreamSynchronize(ctx.stream));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(host_out, ctx.trace.p, static_cast<size_t>(n) * kTraceSlots * 8, cudaMemcpyDeviceToHost));
+    });
+}

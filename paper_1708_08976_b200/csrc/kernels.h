@@ -31,6 +31,32 @@ inline void once_on_device(std::atomic<unsigned long long>& mask, F&& f) {
 constexpr int kLoopMax = 16;
 void launch_loop_sum(double* const* bufs, int P, long long n, double* out, cudaStream_t s);
 
+// Fused cross-rank reduction over peer memory (xrank.cu).
+// One rank's side of a launch: the local values (a plain buffer, or the CSR
+// slot workspace of a streaming MTTKRP when rowptr is set), the output and
+// the rank's per-block epoch counters.
+struct XrankLocal {
+    const double* src;
+    const long long* rowptr;
+    const long long* slots;
+    double* out;
+    unsigned long long* ctr;
+};
+// recv[k] / flags[k]: rank k's receive buffer [2][P][cap] and flag array
+// [P][nblk_cap], mapped into this process (peer pointers, or one device's
+// buffers for the emulated group). me[v]: virtual rank rank0 + v's side.
+struct XrankArgs {
+    int P, rank0, C;
+    long long rows, cap, nblk_cap;
+    double* recv[kLoopMax];
+    unsigned long long* flags[kLoopMax];
+    XrankLocal me[kLoopMax];
+};
+// grid = nblk x vranks (vranks > 1: the emulated group, all ranks in one
+// cooperative launch); rows x C values, rows * C <= cap, nblk <= nblk_cap.
+cudaError_t launch_xrank_reduce(const XrankArgs& a, int nblk, int vranks, cudaStream_t s);
+int xrank_max_blocks();  // co-resident blocks of the kernel on the current device
+
 void launch_krp_level(const double* P, const double* U, double* out, long long rows_out, long long J, int C,
                       cudaStream_t s);
 void launch_mttkrp_generic(const double* X, long long L, long long I, long long R, int C, const KrpGen& kl,

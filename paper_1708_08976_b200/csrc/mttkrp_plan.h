@@ -82,6 +82,19 @@ struct TcPlan {
                               // the others only their own (fewer live registers in the consumer loop)
     int x_wait;               // 1: X is a scratch buffer an earlier kernel wrote (the baseline's
                               // matricised copy): the producer waits for it too (pdl_wait)
+    unsigned long long* trace;  // developer timeline (DMTK_GPU_TRACE): kTraceSlots stamps per CTA, or null
+    int m3;                   // M-major: the tensor map is the 3-D view (16 m, j, m / 16) and one box
+                              // {16, BK, TR / 16} loads a row group's whole stage (else TR / 16 2-D boxes)
+};
+
+// Timeline stamps of the streaming kernel (%globaltimer, ns). Developer tool only.
+constexpr int kTraceStages = 24;  // per-stage stamps of the first stages
+constexpr int kTraceSlots = 16 + 2 * kTraceStages;
+enum TraceEv : int {
+    kTrEntry = 0, kTrPrologue = 1, kTrTmaFirst = 2, kTrTmaLast = 3, kTrBuildFirst = 4, kTrBuildLast = 5,
+    kTrConsFirst = 6, kTrConsLoop = 7, kTrConsEpi = 8, kTrCons7Loop = 9, kTrExit = 10,
+    kTrStageIssue = 16,                   // producer: stage k's loads issued
+    kTrStageReady = 16 + kTraceStages,    // observer: stage k's full barrier complete
 };
 
 // Epilogue instantiations of the streaming kernel (template parameter EPI).

@@ -110,6 +110,16 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // developer timeline (p.trace): %globaltimer stamps (ns; the pointer
+    // stays in the parameter bank, no live registers)
+    auto stamp = [&](int ev) {
+        if (p.trace) {
+            unsigned long long gt;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+            p.trace[static_cast<long long>(blockIdx.x) * kTraceSlots + ev] = gt;
+        }
+    };
+    if (threadIdx.x == 0) stamp(kTrEntry);
     // shared-window addresses, computed once (no per-stage address conversion)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
     if (threadIdx.x == 0) {
@@ -122,6 +132,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     }
     if (warp == kProducerWarp && lane == 0 && !p.ldgsts) tma_prefetch_desc(&tmap);
     __syncthreads();
+    if (threadIdx.x == 0) stamp(kTrPrologue);
     // Programmatic dependent launch: the producer streams X (never written by
     // the library's kernels) without waiting for the previous kernel unless X
     // is a buffer that kernel may have just produced (x_wait); the builders
@@ -230,6 +241,8 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     continue;
                 }
                 mbar_arrive_expect_tx_a(full_a + 8 * slot, Cfg::A_BYTES);
+                if (gs == lo) stamp(kTrTmaFirst);
+                if (gs - lo < kTraceStages) stamp(kTrStageIssue + static_cast<int>(gs - lo));
                 const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
                 if (!KMAJ) {
                     // BM / 16 boxes {16 m, BK j} of 128 * BK bytes: group gi's
@@ -238,9 +251,16 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     const int j0 = static_cast<int>(st * BK * G);
                     const int bpg = p.TR / 16;
                     uint32_t d = dst;
-                    for (int gi = 0; gi < G; ++gi)
-                        for (int bb = 0; bb < bpg; ++bb, d += 128 * BK)
-                            tma_load_2d(d, &tmap, full_a + 8 * slot, m0 + 16 * bb, j0 + BK * gi, pol);
+                    if (p.m3) {
+                        // one 3-D box per row group: the box's 16-row blocks land
+                        // in the same [block][j][16 m] order as the 2-D boxes
+                        for (int gi = 0; gi < G; ++gi, d += bpg * 128 * BK)
+                            tma_load_3d(d, &tmap, full_a + 8 * slot, 0, j0 + BK * gi, m0 >> 4, pol);
+                    } else {
+                        for (int gi = 0; gi < G; ++gi)
+                            for (int bb = 0; bb < bpg; ++bb, d += 128 * BK)
+                                tma_load_2d(d, &tmap, full_a + 8 * slot, m0 + 16 * bb, j0 + BK * gi, pol);
+                    }
                 } else {
                     long long ti, tj, j, l0;
                     if (p.flavor == kKMajorJ) {
@@ -264,9 +284,19 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     }
                     }
                 }
+            stamp(kTrTmaLast);
+        } else if (lane == 1 && p.trace) {
+            // timeline observer: when each of the first stages' full barrier
+            // (TMA bytes + B tile) completes -- waits only, never arrives
+            StageCursor cur;
+            cur.init(lo, spt);
+            for (long long gs = lo; gs < hi && gs - lo < kTraceStages; ++gs, cur.next(spt, STAGES)) {
+                mbar_wait_a(full_a + 8 * cur.slot, cur.ph);
+                stamp(kTrStageReady + static_cast<int>(gs - lo));
             }
-            return;
         }
+        return;
+    }
 
     // ------------------------------------------------------------ builders
     // Work items are (stage, row group) pairs dealt round-robin to the
@@ -457,7 +487,10 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive_a(full_a + 8 * slot);
+                if (lane == 0) {
+                    mbar_arrive_a(full_a + 8 * slot);
+                    if (bw == 0) stamp(gs == lo ? kTrBuildFirst : kTrBuildLast);
+                }
             }
         }
         return;
@@ -577,6 +610,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         mbar_wait_a(full_a, 0u);
         load(f0, 0, 0);
     }
+    if (lane == 0 && w == 0) stamp(kTrConsFirst);
     for (long long gs = lo; gs < hi; ++tile, st0 = 0, ++seg) {
         const int nseg = static_cast<int>(spt - st0 < hi - gs ? spt - st0 : hi - gs);
         gs += nseg;
@@ -614,6 +648,8 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             slot = nslot;
             ph = nph;
         }
+        if (lane == 0 && w == 0) stamp(kTrConsLoop);
+        if (lane == 0 && w == kConsumerWarps - 1) stamp(kTrCons7Loop);
         if (p.debug & 8) {  // experiment: drop the epilogue entirely
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb)
@@ -813,21 +849,21 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                 const long long tj = div_nn(tile, p.n_ti);
                 const long long ti = tile - tj * p.n_ti;
                 if (p.BI >= RW) {
-#pragma unroll
-                    for (int r0 = 0; r0 < RW; r0 += EC) {
-                        double sc[EC];
-                        bool ok[EC];
-#pragma unroll
-                        for (int r = 0; r < EC; ++r) {
-                            const int rho = RW * lw + r0 + r;
-                            const long long i = ti * p.BI + rho % p.BI;
-                            const long long j = tj * p.BJ + rho / p.BI;
-                            ok[r] = i < p.I && j < p.R;
-                            sc[r] = ok[r] ? krp_scale(p.sgen, j, c) : 0.0;
-                        }
-#pragma unroll
-                        for (int r = 0; r < EC; ++r)
-                            if (ok[r]) wsb[(r0 + r) * C + c] = Pw[(r0 + r) * LD + c] * sc[r];
+                    // the warp's rows (i, j) change j at most once (BI >= RW):
+                    // two scale rows, one division per warp
+                    const int rho0 = RW * lw;
+                    const int q0 = rho0 / p.BI;
+                    const int rw = p.BI - (rho0 - q0 * p.BI);  // rows before j + 1
+                    const long long ib = ti * p.BI + (rho0 - q0 * p.BI);
+                    const long long j0 = tj * p.BJ + q0;
+                    const double sc0 = j0 < p.R ? krp_scale(p.sgen, j0, c) : 0.0;
+                    const double sc1 = (rw < RW && j0 + 1 < p.R) ? krp_scale(p.sgen, j0 + 1, c) : 0.0;
+#pragma unroll 8
+                    for (int r = 0; r < RW; ++r) {
+                        const bool first = r < rw;
+                        const long long i = first ? ib + r : ti * p.BI + (r - rw);
+                        const bool ok = i < p.I && (first ? j0 : j0 + 1) < p.R;
+                        if (ok) wsb[r * C + c] = Pw[r * LD + c] * (first ? sc0 : sc1);
                     }
                 } else {
                     const int njl = RW / p.BI;
@@ -857,7 +893,9 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
             for (int tc = 0; tc < (TAIL > 0 ? TAIL : 1); ++tc) tacc[0][rb][tc] = tacc[1][rb][tc] = 0.0;
         }
+        if (lane == 0 && w == 0) stamp(kTrConsEpi);
     }
+    if (lane == 0 && w == 0) stamp(kTrExit);
 }
 
 }  // namespace dmtkg

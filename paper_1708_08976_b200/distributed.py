@@ -76,7 +76,37 @@ def _lib():
 
 
 # ------------------------------------------------------------ communicators
-class DeviceComm:
+class _CommOps:
+    """Exchange queries shared by both communicator kinds."""
+
+    @property
+    def fused(self) -> bool:
+        """True when the exchanges run over peer memory (csrc/xrank.cu)."""
+        C = self._C
+        r, w, f = C.c_int(), C.c_int(), C.c_int()
+        _check(self._lib, self._lib.dmtk_gpu_comm_info(self.handle, C.byref(r), C.byref(w), C.byref(f)))
+        return bool(f.value)
+
+    def mttkrp(self, slab, device_factor_ptrs, rank: int, mode: int, device_out_ptr: int, stream: int = 0,
+               algo: int = 3, order: int = 0):
+        """dmtk_gpu_mttkrp_sharded: this rank's slab; modes < N-1 return the
+        full result summed over the ranks (fused into the MTTKRP's slot
+        reduction with the peer exchange), the last mode this rank's rows.
+        algo/order: MttkrpAlgo / TwoStepOrder values (default automatic)."""
+        C = self._C
+        arr = (C.c_void_p * len(device_factor_ptrs))(*[C.c_void_p(p) for p in device_factor_ptrs])
+        _check(self._lib, self._lib.dmtk_gpu_mttkrp_sharded(self.handle, slab.handle(), arr, int(rank), int(mode),
+                                                            int(algo), int(order), C.c_void_p(device_out_ptr),
+                                                            C.c_void_p(stream or None)))
+
+    def allreduce(self, device_ptr: int, n: int, stream: int = 0):
+        """In-place sum of n doubles at device_ptr over the ranks
+        (dmtk_gpu_comm_allreduce); rank-order sum with the peer exchange."""
+        _check(self._lib, self._lib.dmtk_gpu_comm_allreduce(self.handle, self._C.c_void_p(device_ptr), int(n),
+                                                            self._C.c_void_p(stream or None)))
+
+
+class DeviceComm(_CommOps):
     """An NCCL communicator owned by the library (dmtk_gpu_comm_*): rank 0
     makes the 128-byte id, torch.distributed broadcasts it, every rank joins
     on its device. The library then all-reduces on its own stream, inside the
@@ -110,7 +140,7 @@ class DeviceComm:
             pass
 
 
-class LoopbackComm:
+class LoopbackComm(_CommOps):
     """Rank `rank` of a loopback group (dmtk_gpu_comm_loopback)."""
 
     def __init__(self, handle, rank: int, world: int, device: int):
@@ -178,7 +208,7 @@ def dist_cp_als_device(slab_tensor, comm, global_last: int, last_lo: int, config
                             bool(zero.value))
 
 
-def loopback_cp_als(tensor, world: int, config, packed: bool = False):
+def loopback_cp_als(tensor, world: int, config, packed: bool = False, comms=None):
     """dmtk_gpu_cp_als_sharded over `world` loopback ranks of one device: the
     tensor is cut into its last-mode slabs (dmtk_gpu_tensor_slab), every rank
     runs the production sharded sweep in its own thread, and the exchanges go
@@ -186,7 +216,9 @@ def loopback_cp_als(tensor, world: int, config, packed: bool = False):
     symmetric slices (dmtk_gpu_tensor_pack_sym01) first. Returns the per-rank
     results and the full last factor assembled from the ranks' rows."""
     dims = tensor.dims
-    comms = loopback_comms(world, tensor.device)
+    own = comms is None
+    if own:
+        comms = loopback_comms(world, tensor.device)
     slabs, spans = [], []
     for r in range(world):
         lo, hi = shard_bounds(dims[-1], world, r)
@@ -213,8 +245,9 @@ def loopback_cp_als(tensor, world: int, config, packed: bool = False):
         t.join()
     for s in slabs:
         s.release()
-    for c in comms:
-        c.close()
+    if own:
+        for c in comms:
+            c.close()
     for e in errors:
         if e is not None:
             raise e

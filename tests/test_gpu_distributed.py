@@ -42,18 +42,27 @@ def group():
 
 
 @pytest.mark.parametrize("dims,C", [((6, 5, 7), 4), ((9, 3, 4, 5), 3), ((40, 40, 12, 8), 20)])
-def test_device_sharded_cp_als_world1(group, oracle, dims, C):
+@pytest.mark.parametrize("exchange", ["xrank", "nccl"])
+def test_device_sharded_cp_als_world1(group, oracle, dims, C, exchange):
     """dmtk_gpu_cp_als_sharded with a library-owned NCCL communicator (world 1
     here): every exchange point (MTTKRP partials, the last factor's column
-    norms and Gram, the fit's inner product, ||X||^2) runs as an NCCL
-    all-reduce inside the per-mode CUDA graphs; with one rank the result must
+    norms and Gram, the fit's inner product, ||X||^2) runs inside the per-mode
+    CUDA graphs, as the fused peer-memory exchange kernel (the real, one-rank
+    launch of csrc/xrank.cu: the partials' slot reduction is the exchange) or
+    as an NCCL all-reduce (DMTK_GPU_XRANK=0); with one rank the result must
     equal the single-GPU cp_als and the reference."""
     import paper_1708_08976_b200 as dg
     from paper_1708_08976_b200.distributed import DeviceComm, dist_cp_als_device
 
     x = oracle.gen_tensor(dims, 5)
     t = dg.DenseTensor(dims, x)
-    comm = DeviceComm(0)
+    if exchange == "nccl":
+        os.environ["DMTK_GPU_XRANK"] = "0"
+    try:
+        comm = DeviceComm(0)
+    finally:
+        os.environ.pop("DMTK_GPU_XRANK", None)
+    assert comm.fused == (exchange == "xrank")
     cfg = dg.AlsConfig(rank=C, max_iters=8, tol=0.0, seed=11)
     res = dist_cp_als_device(t, comm, dims[-1], 0, cfg)
     one = dg.cp_als(t, cfg)
@@ -209,3 +218,161 @@ def test_slab_validation(oracle):
         t.slab(4, 7)
     with pytest.raises(dg.OutOfRange):
         t.slab(3, 3)
+
+
+def _run_ranks(P, fn):
+    import threading
+    errs = [None] * P
+
+    def go(r):
+        try:
+            fn(r)
+        except Exception as e:  # surfaced below
+            errs[r] = e
+
+    ts = [threading.Thread(target=go, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("P", [1, 2, 3, 8, 16])
+def test_loopback_fused_exchange_allreduce(P):
+    """The fused peer-memory exchange (csrc/xrank.cu) through
+    dmtk_gpu_comm_allreduce on P loopback ranks (all ranks in one cooperative
+    launch): every rank gets the rank-order sum, bitwise equal to the left fold
+    b_0 + b_1 + ... + b_{P-1} on the host and the same on every rank; sizes from
+    1 to above the receive capacity (chunked), each exchanged three times in a
+    row (epoch parity reuse of the receive rows)."""
+    from paper_1708_08976_b200.distributed import loopback_comms
+    comms = loopback_comms(P)
+    try:
+        assert all(c.fused for c in comms)
+        sizes = [1, 7, 1000, 20000, (1 << 18) + 5]
+        g = torch.Generator().manual_seed(P)
+        host = [[torch.randn(n, dtype=torch.float64, generator=g) for n in sizes] for _ in range(P)]
+        dev = [[h.cuda() for h in row] for row in host]
+        torch.cuda.synchronize()
+        rounds = 3
+
+        def work(r):
+            for _ in range(rounds):
+                for b in dev[r]:
+                    comms[r].allreduce(b.data_ptr(), b.numel())
+
+        _run_ranks(P, work)
+        torch.cuda.synchronize()
+        for i, n in enumerate(sizes):
+            want = [host[r][i].numpy().copy() for r in range(P)]
+            for _ in range(rounds):
+                acc = want[0].copy()
+                for r in range(1, P):
+                    acc = acc + want[r]
+                want = [acc] * P
+            for r in range(P):
+                got = dev[r][i].cpu().numpy()
+                assert np.array_equal(got, want[0]), (P, n, r)
+    finally:
+        for c in comms:
+            c.close()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("dims,C,P,tree", [((40, 40, 12, 8), 20, 3, False), ((20, 18, 17), 9, 8, False),
+                                           ((9, 3, 4, 5), 3, 2, True), ((40, 40, 12, 8), 20, 8, True)])
+def test_loopback_fused_vs_event_exchange(oracle, dims, C, P, tree):
+    """The sharded CP-ALS with the fused exchange (each non-last mode's slot
+    reduction sums the ranks' partials in the same kernel) against the
+    stream-event all-reduce path (DMTK_GPU_XRANK=0): fits within 1e-12 and
+    factors within 1e-12; the fused factors are bitwise identical on every
+    rank and bitwise repeatable on a second run over the same communicators
+    (the exchange epochs carry over)."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import loopback_comms
+    x = oracle.gen_tensor(dims, 5)
+    t = dg.DenseTensor(dims, x)
+    cfg = dg.AlsConfig(rank=C, max_iters=5, tol=0.0, seed=11, dimension_tree=tree)
+    comms = loopback_comms(P)
+    try:
+        assert all(c.fused for c in comms)
+        res, last = loopback_cp_als(t, P, cfg, comms=comms)
+        res2, last2 = loopback_cp_als(t, P, cfg, comms=comms)
+    finally:
+        for c in comms:
+            c.close()
+    os.environ["DMTK_GPU_XRANK"] = "0"
+    try:
+        ev = loopback_comms(P)
+        assert not any(c.fused for c in ev)
+        for c in ev:
+            c.close()
+        ref_res, ref_last = loopback_cp_als(t, P, cfg)
+    finally:
+        del os.environ["DMTK_GPU_XRANK"]
+    for r in range(P):
+        assert np.max(np.abs(np.array(res[r].fits) - np.array(ref_res[r].fits))) <= 1e-12
+        for a, b in zip(res[r].factors[:-1], ref_res[r].factors[:-1]):
+            assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+        for a, b in zip(res[r].factors, res[0].factors[:-1]):
+            assert np.array_equal(a, b)
+        for a, b in zip(res[r].factors, res2[r].factors):
+            assert np.array_equal(a, b)
+        assert res[r].fits == res2[r].fits
+    assert np.linalg.norm(last - ref_last) <= 1e-12 * np.linalg.norm(ref_last)
+    assert np.array_equal(last, last2)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("dims,C,P", [((30, 20, 17), 9, 3), ((12, 10, 9, 8), 25, 2), ((40, 40, 12, 8), 20, 8),
+                                      ((200, 200, 200), 16, 3)])
+def test_loopback_mttkrp_sharded(oracle, dims, C, P):
+    """dmtk_gpu_mttkrp_sharded on P loopback ranks (the fused peer-memory
+    exchange: each non-last mode's slot reduction sums the ranks' partials):
+    modes < N-1 give the full MTTKRP on every rank, bitwise the same on all
+    ranks and within 1e-12 of the single-device result; the last mode gives
+    each rank its rows. Every mode twice in a row (exchange epochs)."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import loopback_comms
+    x = oracle.gen_tensor(dims, 3)
+    f = oracle.gen_factors(dims, C, 4)
+    t = dg.DenseTensor(dims, x)
+    N = len(dims)
+    want = [dg.mttkrp(dg.MttkrpRequest(t, f, m)).m for m in range(N)]
+    comms = loopback_comms(P)
+    slabs, outs, facs = [], [], []
+    try:
+        for r in range(P):
+            lo, hi = shard_bounds(dims[-1], P, r)
+            slabs.append(t.slab(lo, hi))
+            fr = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in f[:-1]]
+            fr.append(torch.from_numpy(np.ascontiguousarray(f[-1][lo:hi])).cuda())
+            facs.append(fr)
+            outs.append([torch.zeros((dims[m] if m < N - 1 else hi - lo, C), dtype=torch.float64, device="cuda")
+                         for m in range(N)])
+        torch.cuda.synchronize()
+
+        def work(r):
+            for _ in range(2):
+                for m in range(N):
+                    comms[r].mttkrp(slabs[r], [a.data_ptr() for a in facs[r]], C, m, outs[r][m].data_ptr())
+            torch.cuda.synchronize()
+
+        _run_ranks(P, work)
+        torch.cuda.synchronize()
+        for m in range(N - 1):
+            got0 = outs[0][m].cpu().numpy()
+            assert np.linalg.norm(got0 - want[m]) <= 1e-12 * np.linalg.norm(want[m]), m
+            for r in range(1, P):
+                assert np.array_equal(outs[r][m].cpu().numpy(), got0), (m, r)
+        last = np.concatenate([outs[r][N - 1].cpu().numpy() for r in range(P)], axis=0)
+        assert np.linalg.norm(last - want[N - 1]) <= 1e-12 * np.linalg.norm(want[N - 1])
+    finally:
+        for s in slabs:
+            s.release()
+        for c in comms:
+            c.close()

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--modes", default="")
+    ap.add_argument("--flush", action="store_true")
     args = ap.parse_args()
     libs = [load(args.a), load(args.b)]
     for cfg in args.config.split(","):
@@ -77,8 +78,21 @@ def main():
                 c()
             torch.cuda.synchronize()
             ts = [[], []]
+            junk = torch.empty(64 << 20, dtype=torch.float64, device="cuda") if args.flush else None
             for _ in range(args.rounds):
                 for k, c in enumerate(calls):
+                    if junk is not None:  # L2 flush before every timed call (as bench.py's 200c16 block)
+                        tot = 0.0
+                        for _ in range(args.reps):
+                            junk.fill_(1.0)
+                            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            e0.record()
+                            c()
+                            e1.record()
+                            torch.cuda.synchronize()
+                            tot += e0.elapsed_time(e1)
+                        ts[k].append(tot / args.reps)
+                        continue
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
                     for _ in range(args.reps):
@@ -86,6 +100,7 @@ def main():
                     e1.record()
                     torch.cuda.synchronize()
                     ts[k].append(e0.elapsed_time(e1) / args.reps)
+            del junk
             ma, mb = statistics.median(ts[0]), statistics.median(ts[1])
             print(json.dumps({"config": cfg, "mode": mode, "a_ms": round(ma, 4), "b_ms": round(mb, 4),
                               "b_speedup_pct": round(100 * (ma / mb - 1), 2),

@@ -37,7 +37,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--bw", type=float, default=6455.9)
     ap.add_argument("--modes", default="")
+    ap.add_argument("--flush", action="store_true", help="write 512 MB before every timed call (L2 flush, as bench.py)")
     ap.add_argument("--upload", action="store_true", help="upload through the host API (padded odd layouts)")
+    ap.add_argument("--wrap", action="store_true", help="borrow a torch tensor (dmtk_gpu_tensor_wrap)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up, run one call per mode between cudaProfilerStart/Stop (for ncu "
                          "--profile-from-start off) and skip the timing")
@@ -55,8 +57,13 @@ def main():
         g = torch.Generator(device="cuda").manual_seed(1)
         x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
         fs = [torch.rand((d, C), dtype=torch.float64, device="cuda", generator=g) for d in dims]
-        t = (dg.DenseTensor(dims, x.cpu().numpy()) if args.upload else
-             dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x))
+        if args.upload:
+            t = dg.DenseTensor(dims, x.cpu().numpy())
+        elif args.wrap:
+            t = dg.DenseTensor.from_device(dims, x.data_ptr(), owner=x)
+        else:  # library-owned, as bench.py (dmtk_gpu_tensor_generate)
+            del x
+            t = dg.DenseTensor.generate(dims, 1)
         s = torch.cuda.current_stream()
         modes = [int(m) for m in args.modes.split(",")] if args.modes else range(len(dims))
         modes = [m if m >= 0 else len(dims) + m for m in modes]
@@ -78,20 +85,34 @@ def main():
                     torch.cuda.synchronize()
                     torch.cuda.profiler.stop()
                     continue
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(args.reps):
-                    call()
-                e1.record()
-                torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / args.reps
+                if args.flush:
+                    junk = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
+                    tot = 0.0
+                    for _ in range(args.reps):
+                        junk.fill_(1.0)
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        call()
+                        e1.record()
+                        torch.cuda.synchronize()
+                        tot += e0.elapsed_time(e1)
+                    ms = tot / args.reps
+                    del junk
+                else:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(args.reps):
+                        call()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms = e0.elapsed_time(e1) / args.reps
                 gbs = 8 * n / (ms * 1e-3) / 1e9
                 tfs = 2 * n * C / (ms * 1e-3) / 1e12
                 roof = max(8 * n / (args.bw * 1e9), 2 * n * C / (peak * 1e12))
                 print(json.dumps({"config": cfg, "mode": mode, "algo": an, "ms": round(ms, 4), "GBs": round(gbs, 1),
                                   "TFs": round(tfs, 2), "frac": round(roof / (ms * 1e-3), 3),
                                   "peak_tf": round(peak, 2)}), flush=True)
-        del x, fs, t
+        del fs, t
         torch.cuda.empty_cache()
 
 
