@@ -1966,6 +1966,7 @@ int dmtk_gpu_tensor_slab(dmtk_gpu_tensor t, int64_t lo, int64_t hi, dmtk_gpu_ten
         p->dims[N - 1] = hi - lo;
         p->total = prod(p->dims, 0, N);
         p->pdims = t->pdims;
+        p->pdims[N - 1] = hi - lo;  // the slab's own physical extent (only the first mode is ever padded)
         long long plane = prod(t->pdims, 0, N - 1), first = lo * plane, count = (hi - lo) * plane;
         if (N == 1) {  // a 1-way slab: same layout rule as an upload (even physical extent)
             p->pdims[0] = (hi - lo) + ((hi - lo) & 1);

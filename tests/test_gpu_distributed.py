@@ -376,3 +376,36 @@ def test_loopback_mttkrp_sharded(oracle, dims, C, P):
             s.release()
         for c in comms:
             c.close()
+
+
+@pytest.mark.parametrize("dims,C", [((30, 20, 17), 9), ((7, 6, 5, 9), 4), ((31, 8, 11), 3)])
+def test_slab_is_its_own_extent(oracle, dims, C):
+    """A slab holds only its own last-mode rows: the device-resident MTTKRP of
+    every mode writes exactly its result rows (a guard band after an
+    exactly-sized output stays untouched) and equals the MTTKRP of the slab's
+    bytes uploaded as a tensor of its own."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200 import MttkrpAlgo as A, TwoStepOrder as O
+    x = oracle.gen_tensor(dims, 3)
+    f = oracle.gen_factors(dims, C, 4)
+    t = dg.DenseTensor(dims, x)
+    N = len(dims)
+    plane = int(np.prod(dims[:-1]))
+    for lo, hi in [(0, 2), (2, dims[-1]), (1, dims[-1] - 1)]:
+        s = t.slab(lo, hi)
+        sd = tuple(dims[:-1]) + (hi - lo,)
+        own = dg.DenseTensor(sd, x[lo * plane:hi * plane].copy())
+        fr = f[:-1] + [f[-1][lo:hi]]
+        dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in fr]
+        for m in range(N):
+            rows = sd[m]
+            buf = torch.full((rows * C + 64,), 7.25, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            dg.mttkrp_device(s, [a.data_ptr() for a in dev], C, m, A.automatic, O.automatic, buf.data_ptr(), 0)
+            torch.cuda.synchronize()
+            got = buf.cpu().numpy()
+            assert np.all(got[rows * C:] == 7.25), (lo, hi, m)  # nothing past the result
+            want = dg.mttkrp(dg.MttkrpRequest(own, fr, m)).m
+            assert np.linalg.norm(got[:rows * C].reshape(rows, C) - want) <= 1e-12 * np.linalg.norm(want)
+        s.release()
+        own.release()
