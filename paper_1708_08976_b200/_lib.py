@@ -85,6 +85,7 @@ _SIGS = {
     "dmtk_gpu_fp64_peak_sustained": (C.c_int, [C.c_int, C.c_double, dp]),
     "dmtk_gpu_launch_count": (C.c_int64, []),
     "dmtk_gpu_debug_trace": (C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
+    "dmtk_gpu_debug_cached_shapes": (C.c_int, [C.POINTER(C.c_int64)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -218,6 +218,12 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ double2 lds_v2f64(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

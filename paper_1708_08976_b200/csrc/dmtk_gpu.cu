@@ -644,12 +644,15 @@ static void tc_slots(const TcPlan& p, int grid, std::vector<std::pair<long long,
 }
 
 // Plans and CSR slot maps depend on the tensor's shape and layout, not on
-// its values, so they are cached per (device, shape, layout, alignment) for
-// the whole process: a fresh handle of a known shape (a new upload every
-// call, the drop-in's first call on a new DenseTensor) skips the planning and
-// the slot-map build (1000^3 C=25: 2.2 -> 1.7 ms per host-buffer call). Entries
-// are never dropped (CUDA graphs captured by CP-ALS hold the slot-map
-// pointers); callers hold the device context's mutex.
+// its values, so they are cached per (device, slot, shape, layout,
+// alignment): a fresh handle of a known shape (a new upload every call, the
+// drop-in's first call on a new DenseTensor) skips the planning and the
+// slot-map build (1000^3 C=25: 2.2 -> 1.7 ms per host-buffer call). The cache
+// keeps the kShapeCacheMax most recently used shapes per (device, slot); an
+// older shape is dropped (its slot maps freed) when a new one arrives, unless
+// a running CP-ALS pins it (its CUDA graphs hold the slot-map pointers).
+// Callers hold the slot's context mutex, so a shape is never dropped while
+// the same slot is using it.
 struct ShapeKey {
     int device, slot;
     std::vector<long long> dims, pdims;
@@ -664,18 +667,64 @@ static ShapeKey shape_key(const dmtk_gpu_tensor_s& t) {
     return ShapeKey{t.device, g_slot, t.dims, t.pdims, t.sym01, (reinterpret_cast<uintptr_t>(t.d) & 15) == 0};
 }
 
+constexpr size_t kShapeCacheMax = 64;
+struct ShapeCacheEntry {
+    std::map<long long, std::unique_ptr<PlanCacheEntry>> plans;
+    std::map<std::pair<PlanKey, long long>, std::unique_ptr<CsrPlan>> csrs;
+    unsigned long long last_use = 0;
+    int pins = 0;
+};
+static std::mutex g_shape_mu;
+static std::map<ShapeKey, std::unique_ptr<ShapeCacheEntry>> g_shapes;
+static unsigned long long g_shape_tick = 0;
+
+static ShapeCacheEntry& shape_entry(const dmtk_gpu_tensor_s& t) {
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    const ShapeKey key = shape_key(t);
+    auto it = g_shapes.find(key);
+    if (it == g_shapes.end()) {
+        // evict the least recently used unpinned shape of this (device, slot)
+        size_t same = 0;
+        auto victim = g_shapes.end();
+        for (auto jt = g_shapes.begin(); jt != g_shapes.end(); ++jt) {
+            if (jt->first.device != key.device || jt->first.slot != key.slot) continue;
+            ++same;
+            if (jt->second->pins == 0 && (victim == g_shapes.end() || jt->second->last_use < victim->second->last_use))
+                victim = jt;
+        }
+        if (same >= kShapeCacheMax && victim != g_shapes.end()) g_shapes.erase(victim);  // frees its slot maps
+        it = g_shapes.emplace(key, std::make_unique<ShapeCacheEntry>()).first;
+    }
+    it->second->last_use = ++g_shape_tick;
+    return *it->second;
+}
+
+static size_t shape_cache_size() {
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    return g_shapes.size();
+}
+
+// Keeps a shape's plans and slot maps alive for a scope (CP-ALS graphs).
+struct ShapePin {
+    ShapeCacheEntry* e;
+    explicit ShapePin(const dmtk_gpu_tensor_s& t) : e(&shape_entry(t)) {
+        std::lock_guard<std::mutex> lk(g_shape_mu);
+        ++e->pins;
+    }
+    ~ShapePin() {
+        std::lock_guard<std::mutex> lk(g_shape_mu);
+        --e->pins;
+    }
+    ShapePin(const ShapePin&) = delete;
+    ShapePin& operator=(const ShapePin&) = delete;
+};
+
 static std::map<long long, std::unique_ptr<PlanCacheEntry>>& plans_of(const dmtk_gpu_tensor_s& t) {
-    static std::mutex mu;
-    static std::map<ShapeKey, std::map<long long, std::unique_ptr<PlanCacheEntry>>> m;
-    std::lock_guard<std::mutex> lk(mu);
-    return m[shape_key(t)];
+    return shape_entry(t).plans;
 }
 
 static std::map<std::pair<PlanKey, long long>, std::unique_ptr<CsrPlan>>& csrs_of(const dmtk_gpu_tensor_s& t) {
-    static std::mutex mu;
-    static std::map<ShapeKey, std::map<std::pair<PlanKey, long long>, std::unique_ptr<CsrPlan>>> m;
-    std::lock_guard<std::mutex> lk(mu);
-    return m[shape_key(t)];
+    return shape_entry(t).csrs;
 }
 
 static CsrPlan& csr_for(dmtk_gpu_tensor_s& t, int mode, int C, const ModePlan& mp, Context& ctx) {
@@ -2500,6 +2549,7 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         cudaStream_t s = ctx.stream;
 
         if (!t->sym01) ensure_layout(*t, ctx, s);
+        const ShapePin pin(*t);  // the iteration graphs hold this shape's slot maps
         // factor rows on the device: the physical extents (a padded first
         // factor), or the logical ones for a packed symmetric tensor
         const std::vector<long long> frows = t->sym01 ? t->dims : t->pdims;
@@ -3388,5 +3438,12 @@ int dmtk_gpu_debug_trace(int device, uint64_t* host_out, int max_ctas, int* n_ct
         CK(cudaStreamSynchronize(ctx.stream));
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(host_out, ctx.trace.p, static_cast<size_t>(n) * kTraceSlots * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int dmtk_gpu_debug_cached_shapes(int64_t* n) {
+    return guarded([&] {
+        if (!n) fail(DMTK_GPU_EINVAL, "debug_cached_shapes: null argument");
+        *n = static_cast<int64_t>(shape_cache_size());
     });
 }

@@ -530,6 +530,10 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 
     double acc[RB][NB][2];
     // tail accumulators split by k4-step parity: two independent DFMA chains
+#ifndef DMTK_TAIL_CHAINS
+#define DMTK_TAIL_CHAINS 2
+#endif
+    constexpr int kTailChains = DMTK_TAIL_CHAINS;
     double tacc[2][RB][TAIL > 0 ? TAIL : 1];
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb) {
@@ -553,12 +557,16 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     };
     const uint32_t a_warp = KMAJ ? static_cast<uint32_t>(gi * (Cfg::A_BYTES / G) + (RW * lw + gl) * 128) : 0u;
     const uint32_t a_box = KMAJ ? static_cast<uint32_t>(Cfg::A_BYTES / G / (BK / 16)) : 0u;
+    // Fragment loads by 32-bit shared-window addresses (ld.shared): the
+    // generic-pointer form made the compiler rebuild the CTA's shared window
+    // base (S2R SR_CgaCtaId + LEA) at the top of every stage.
+    const uint32_t sB_lane = smem_u32(sB) + gi * Cfg::B_BYTES + (lane << 4);
+    const uint32_t sT_lane = smem_u32(sB) + gi * Cfg::B_BYTES + Cfg::BMAIN * 8 + tl * (TAIL > 0 ? TAIL : 1) * 8;
     auto load = [&](Frag& f, int sl, int s2) {
-        const unsigned char* As = sA + sl * Cfg::A_BYTES;
-        const double* Bm = reinterpret_cast<const double*>(sB + sl * GB_BYTES + gi * Cfg::B_BYTES);
+        const uint32_t As = sA_a + sl * Cfg::A_BYTES;
+        const uint32_t Bl = sB_lane + sl * GB_BYTES;
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-            f.bv[nb] = *reinterpret_cast<const double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1));
+        for (int nb = 0; nb < NB; ++nb) f.bv[nb] = lds_v2f64(Bl + (s2 * NB + nb) * 512);
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
             const int s = 2 * s2 + sub;
@@ -566,12 +574,12 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             for (int rb = 0; rb < RB; ++rb) {
                 const uint32_t off = !KMAJ ? (s >> 1) * 1024 + aoff[2 * rb + (s & 1)]
                                            : a_warp + (s >> 2) * a_box + 8 * rb * 128 + aoff[s & 3];
-                f.a[sub][rb] = *reinterpret_cast<const double*>(As + off);
+                f.a[sub][rb] = lds_f64(As + off);
             }
             if (TAIL > 0) {
-                const double* Bt = Bm + Cfg::BMAIN;
 #pragma unroll
-                for (int tc = 0; tc < TAIL; ++tc) f.bt[sub][tc] = Bt[(s * 4 + tl) * (TAIL > 0 ? TAIL : 1) + tc];
+                for (int tc = 0; tc < TAIL; ++tc)
+                    f.bt[sub][tc] = lds_f64(sT_lane + sl * GB_BYTES + (s * 4 * (TAIL > 0 ? TAIL : 1) + tc) * 8);
             }
         }
     };
@@ -589,7 +597,8 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                 for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
                     for (int tc = 0; tc < TAIL; ++tc)
-                        tacc[sub][rb][tc] = fma(f.a[sub][rb], f.bt[sub][tc], tacc[sub][rb][tc]);
+                        tacc[sub & (kTailChains - 1)][rb][tc] =
+                            fma(f.a[sub][rb], f.bt[sub][tc], tacc[sub & (kTailChains - 1)][rb][tc]);
                 }
             }
         }

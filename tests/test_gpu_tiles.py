@@ -235,3 +235,32 @@ def test_results_identical_across_processes(tmp_path):
         assert r.returncode == 0, r.stderr[-3000:]
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_shape_cache_is_bounded(oracle):
+    """Plans and slot maps are cached per shape, at most 64 shapes per device
+    and execution slot (least recently used dropped, slot maps freed): 80
+    distinct shapes in a row keep the cache bounded, and a dropped shape
+    re-plans to the same result (bitwise)."""
+    import ctypes as C
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200._lib import lib
+
+    first = None
+    for k in range(80):
+        dims = (6 + k % 7, 5 + k // 7, 4 + (k * 3) % 5)
+        x = oracle.gen_tensor(dims, 11 + k)
+        f = oracle.gen_factors(dims, 3, 12 + k)
+        t = dg.DenseTensor(dims, x)
+        got = dg.mttkrp(dg.MttkrpRequest(t, f, 1)).m
+        if k == 0:
+            first = (dims, x, f, got)
+        t.release()
+    n = C.c_int64(0)
+    assert lib.dmtk_gpu_debug_cached_shapes(C.byref(n)) == 0
+    assert n.value <= 64
+    dims, x, f, want = first  # evicted by now: planned again
+    t = dg.DenseTensor(dims, x)
+    assert np.array_equal(dg.mttkrp(dg.MttkrpRequest(t, f, 1)).m, want)
+    t.release()
+
