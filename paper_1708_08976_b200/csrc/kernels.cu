@@ -259,17 +259,16 @@ __global__ void mttkrp_generic_kernel(const double* __restrict__ X, long long L,
 
 // ------------------------------------------------------------ CSR reduce
 // out(i, c) = sum_{e in [rowptr[i], rowptr[i+1])} ws(slot[e], c), fixed order.
-// One CTA per output row: thread (p, c) sums slots k = p, p + P, ... of the
-// row's CSR range for column c (coalesced over c), then the P partials are
-// added in a fixed order: deterministic, and the row's slots are read by
-// P independent load streams instead of one dependent chain.
+// One CTA per output row: thread (p, c) sums slots k = p + P (4 j + q) of the
+// row's CSR range for column c (coalesced over c) in four independent chains
+// q (a serial FP64 add chain costs ~100 cycles per link on B200, and each
+// link waits on two dependent loads), the chains and then the P partials
+// added in a fixed order: deterministic, with 4 P load streams per row.
 constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const double* __restrict__ ws,
                                                                      const long long* __restrict__ rowptr,
                                                                      const long long* __restrict__ slots, int C,
                                                                      double* __restrict__ out) {
-    pdl_wait();
-    pdl_trigger();
     __shared__ double part[kReduceThreads];
     pdl_wait();  // the slots are the streaming kernel's output
     pdl_trigger();
@@ -279,13 +278,26 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
     const int c = threadIdx.x - p * C;
     const long long k0 = rowptr[i], k1 = rowptr[i + 1];
     double s = 0.0;
-    if (p < P)
-        for (long long k = k0 + p; k < k1; k += P) s += ws[slots[k] * C + c];
+    if (p < P) {
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+        long long k = k0 + p;
+        for (; k + 3 * P < k1; k += 4 * P) {
+            const long long e0 = slots[k], e1 = slots[k + P], e2 = slots[k + 2 * P], e3 = slots[k + 3 * P];
+            q[0] += ws[e0 * C + c];
+            q[1] += ws[e1 * C + c];
+            q[2] += ws[e2 * C + c];
+            q[3] += ws[e3 * C + c];
+        }
+        if (k < k1) q[0] += ws[slots[k] * C + c];  // at most three left
+        if (k + P < k1) q[1] += ws[slots[k + P] * C + c];
+        if (k + 2 * P < k1) q[2] += ws[slots[k + 2 * P] * C + c];
+        s = (q[0] + q[1]) + (q[2] + q[3]);
+    }
     part[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x < C) {
         double t = 0.0;
-        for (int q = 0; q < P; ++q) t += part[q * C + threadIdx.x];
+        for (int r = 0; r < P; ++r) t += part[r * C + threadIdx.x];
         out[i * C + threadIdx.x] = t;
     }
 }
@@ -295,8 +307,6 @@ __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const doubl
 __global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
                                         const long long* __restrict__ slots, long long rows, int C,
                                         double* __restrict__ out) {
-    pdl_wait();
-    pdl_trigger();
     pdl_wait();
     pdl_trigger();
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;

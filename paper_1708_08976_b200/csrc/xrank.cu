@@ -83,8 +83,22 @@ __global__ void __launch_bounds__(kXThreads) xrank_reduce_kernel(const XrankArgs
         for (long long i = r0; i < r1; ++i) {
             const long long k0 = me.rowptr[i], k1 = me.rowptr[i + 1];
             double s = 0.0;
-            if (p < Q)
-                for (long long k = k0 + p; k < k1; k += Q) s += me.src[me.slots[k] * C + c];
+            if (p < Q) {  // four independent chains, as slot_reduce_kernel
+                double q[4] = {0.0, 0.0, 0.0, 0.0};
+                long long k = k0 + p;
+                for (; k + 3 * Q < k1; k += 4 * Q) {
+                    const long long e0 = me.slots[k], e1 = me.slots[k + Q], e2 = me.slots[k + 2 * Q],
+                                    e3 = me.slots[k + 3 * Q];
+                    q[0] += me.src[e0 * C + c];
+                    q[1] += me.src[e1 * C + c];
+                    q[2] += me.src[e2 * C + c];
+                    q[3] += me.src[e3 * C + c];
+                }
+                if (k < k1) q[0] += me.src[me.slots[k] * C + c];  // at most three left
+                if (k + Q < k1) q[1] += me.src[me.slots[k + Q] * C + c];
+                if (k + 2 * Q < k1) q[2] += me.src[me.slots[k + 2 * Q] * C + c];
+                s = (q[0] + q[1]) + (q[2] + q[3]);
+            }
             part[threadIdx.x] = s;
             __syncthreads();
             if (threadIdx.x < C) {
