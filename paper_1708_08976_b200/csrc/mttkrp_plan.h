@@ -108,8 +108,14 @@ enum Epi : int {
 
 // Stage range of CTA b under the stream-K split.
 __host__ __device__ inline void cta_stage_range(long long total, int grid, int b, long long& lo, long long& hi) {
-    lo = total * b / grid;
-    hi = total * (b + 1) / grid;
+    const long long a0 = total * b, a1 = total * (b + 1);
+    if (a1 < 0x7fffffffLL) {  // 32-bit division when it fits (every BASELINE shape)
+        lo = static_cast<unsigned>(a0) / static_cast<unsigned>(grid);
+        hi = static_cast<unsigned>(a1) / static_cast<unsigned>(grid);
+    } else {
+        lo = a0 / grid;
+        hi = a1 / grid;
+    }
 }
 
 }  // namespace dmtkg

@@ -67,7 +67,7 @@ struct StageCursor {
     int slot;
     uint32_t ph;
     __device__ __forceinline__ void init(long long lo, long long spt) {
-        tile = lo / spt;
+        tile = div_nn(lo, spt);
         st = lo - tile * spt;
         slot = 0;
         ph = 0;
@@ -122,6 +122,63 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     if (threadIdx.x == 0) stamp(kTrEntry);
     // shared-window addresses, computed once (no per-stage address conversion)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
+    long long lo, hi;
+    cta_stage_range(p.total_stages, gridDim.x, blockIdx.x, lo, hi);
+    const long long spt = p.stages_per_tile;
+
+    // TMA issue of one stage (the producer lane): expect_tx + the stage's boxes
+    auto issue_stage = [&](const StageCursor& cur, uint64_t pol) {
+        const int slot = cur.slot;
+        const long long tile = cur.tile;
+        const long long st = cur.st;
+        mbar_arrive_expect_tx_a(full_a + 8 * slot, Cfg::A_BYTES);
+        const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
+        if (!KMAJ) {
+            // BM / 16 boxes {16 m, BK j} of 128 * BK bytes: group gi's
+            // boxes cover rows 16 bb of its TR-row tile at j0 + BK gi
+            const int m0 = static_cast<int>(tile * p.TR);
+            const int j0 = static_cast<int>(st * BK * G);
+            const int bpg = p.TR / 16;
+            uint32_t d = dst;
+            if (p.m3) {
+                // one 3-D box per row group: the box's 16-row blocks land
+                // in the same [block][j][16 m] order as the 2-D boxes
+                for (int gi = 0; gi < G; ++gi, d += bpg * 128 * BK)
+                    tma_load_3d(d, &tmap, full_a + 8 * slot, 0, j0 + BK * gi, m0 >> 4, pol);
+            } else {
+                for (int gi = 0; gi < G; ++gi)
+                    for (int bb = 0; bb < bpg; ++bb, d += 128 * BK)
+                        tma_load_2d(d, &tmap, full_a + 8 * slot, m0 + 16 * bb, j0 + BK * gi, pol);
+            }
+        } else {
+            long long ti, tj, j, l0;
+            if (p.flavor == kKMajorJ) {
+                tj = div_nn(tile, p.n_ti);
+                ti = tile - tj * p.n_ti;
+                l0 = st * BK * G;
+                j = tj * p.BJ;
+            } else {
+                ti = tile;
+                j = div_nn(st, p.n_lc);
+                l0 = (st - j * p.n_lc) * BK * G;
+            }
+            // per group: BK / 16 boxes {16 l, BI, BJ} of TR * 128 bytes
+            const int gbytes = Cfg::A_BYTES / G;
+            for (int gi = 0; gi < G; ++gi) {
+#pragma unroll
+                for (int h = 0; h < BK / 16; ++h)
+                    tma_load_3d(dst + gi * gbytes + h * (gbytes / (BK / 16)), &tmap, full_a + 8 * slot,
+                                static_cast<int>(l0 + BK * gi + 16 * h), static_cast<int>(ti * p.BI),
+                                static_cast<int>(j), pol);
+            }
+        }
+    };
+    // The producer lane (thread 0) initialises the barriers and issues the
+    // first ring fill before the CTA barrier: the first stages' DRAM latency
+    // then overlaps the other roles' start-up (their code's first fetch, PDL
+    // wait, builder set-up). The ring slots are empty, so no empty-barrier
+    // wait is needed for them.
+    int pre = 0;  // stages issued here (the producer loop skips them)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             // producer (one expect_tx arrival, or 32 cp.async arrivals) + one per builder item
@@ -129,8 +186,20 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_barrier_init();
+        if (!p.ldgsts) {
+            tma_prefetch_desc(&tmap);
+            if (!p.x_wait && !(p.debug & 2)) {
+                const uint64_t pol = (p.debug & 16) ? l2_evict_normal_policy() : l2_evict_first_policy();
+                StageCursor cur;
+                cur.init(lo, spt);
+                for (long long gs = lo; gs < hi && pre < STAGES; ++gs, ++pre, cur.next(spt, STAGES)) {
+                    issue_stage(cur, pol);
+                    if (pre == 0) stamp(kTrTmaFirst);
+                    if (pre < kTraceStages) stamp(kTrStageIssue + pre);
+                }
+            }
+        }
     }
-    if (warp == kProducerWarp && lane == 0 && !p.ldgsts) tma_prefetch_desc(&tmap);
     __syncthreads();
     if (threadIdx.x == 0) stamp(kTrPrologue);
     // Programmatic dependent launch: the producer streams X (never written by
@@ -142,10 +211,6 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         pdl_wait();
         pdl_trigger();
     }
-
-    long long lo, hi;
-    cta_stage_range(p.total_stages, gridDim.x, blockIdx.x, lo, hi);
-    const long long spt = p.stages_per_tile;
 
     // ------------------------------------------------------------ producer
     if (warp == kProducerWarp && p.ldgsts) {
@@ -232,58 +297,17 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             StageCursor cur;
             cur.init(lo, spt);
             for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
+                if (gs - lo < pre) continue;  // issued in the prologue
                 const int slot = cur.slot;
-                const long long tile = cur.tile;
-                const long long st = cur.st;
                 mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
                 if (p.debug & 2) {
                     mbar_arrive_a(full_a + 8 * slot);
                     continue;
                 }
-                mbar_arrive_expect_tx_a(full_a + 8 * slot, Cfg::A_BYTES);
+                issue_stage(cur, pol);
                 if (gs == lo) stamp(kTrTmaFirst);
                 if (gs - lo < kTraceStages) stamp(kTrStageIssue + static_cast<int>(gs - lo));
-                const uint32_t dst = sA_a + slot * Cfg::A_BYTES;
-                if (!KMAJ) {
-                    // BM / 16 boxes {16 m, BK j} of 128 * BK bytes: group gi's
-                    // boxes cover rows 16 bb of its TR-row tile at j0 + BK gi
-                    const int m0 = static_cast<int>(tile * p.TR);
-                    const int j0 = static_cast<int>(st * BK * G);
-                    const int bpg = p.TR / 16;
-                    uint32_t d = dst;
-                    if (p.m3) {
-                        // one 3-D box per row group: the box's 16-row blocks land
-                        // in the same [block][j][16 m] order as the 2-D boxes
-                        for (int gi = 0; gi < G; ++gi, d += bpg * 128 * BK)
-                            tma_load_3d(d, &tmap, full_a + 8 * slot, 0, j0 + BK * gi, m0 >> 4, pol);
-                    } else {
-                        for (int gi = 0; gi < G; ++gi)
-                            for (int bb = 0; bb < bpg; ++bb, d += 128 * BK)
-                                tma_load_2d(d, &tmap, full_a + 8 * slot, m0 + 16 * bb, j0 + BK * gi, pol);
-                    }
-                } else {
-                    long long ti, tj, j, l0;
-                    if (p.flavor == kKMajorJ) {
-                        tj = div_nn(tile, p.n_ti);
-                        ti = tile - tj * p.n_ti;
-                        l0 = st * BK * G;
-                        j = tj * p.BJ;
-                    } else {
-                        ti = tile;
-                        j = div_nn(st, p.n_lc);
-                        l0 = (st - j * p.n_lc) * BK * G;
-                    }
-                    // per group: BK / 16 boxes {16 l, BI, BJ} of TR * 128 bytes
-                    const int gbytes = Cfg::A_BYTES / G;
-                    for (int gi = 0; gi < G; ++gi) {
-#pragma unroll
-                        for (int h = 0; h < BK / 16; ++h)
-                            tma_load_3d(dst + gi * gbytes + h * (gbytes / (BK / 16)), &tmap, full_a + 8 * slot,
-                                        static_cast<int>(l0 + BK * gi + 16 * h), static_cast<int>(ti * p.BI),
-                                        static_cast<int>(j), pol);
-                    }
-                    }
-                }
+            }
             stamp(kTrTmaLast);
         } else if (lane == 1 && p.trace) {
             // timeline observer: when each of the first stages' full barrier
@@ -612,7 +636,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     // int-counted inner loop: per-stage bookkeeping is a ring-slot step only.
     int slot = 0;
     uint32_t ph = 0;
-    long long tile = lo / spt;
+    long long tile = div_nn(lo, spt);
     long long st0 = lo - tile * spt;
     Frag f0, f1;
     if (kPrefetch && lo < hi) {
