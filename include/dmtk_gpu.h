@@ -307,8 +307,9 @@ int64_t dmtk_gpu_launch_count(void);
  * CTA, 0 = not reached; see TraceEv in csrc/mttkrp_plan.h. Not part of the
  * reference interface. */
 int dmtk_gpu_debug_trace(int device, uint64_t* host_out, int max_ctas, int* n_ctas);
-/* Number of tensor shapes whose plans and CSR slot maps are cached (at most
- * 64 per device and execution slot, least recently used dropped first). */
+/* Number of tensor shapes whose plans and CSR slot maps are cached for the
+ * calling thread's execution slot (at most 64 per device and slot, least
+ * recently used dropped first). */
 int dmtk_gpu_debug_cached_shapes(int64_t* n);
 
 #ifdef __cplusplus

@@ -699,9 +699,11 @@ static ShapeCacheEntry& shape_entry(const dmtk_gpu_tensor_s& t) {
     return *it->second;
 }
 
-static size_t shape_cache_size() {
+static size_t shape_cache_size() {  // shapes cached for the calling thread's execution slot
     std::lock_guard<std::mutex> lk(g_shape_mu);
-    return g_shapes.size();
+    size_t n = 0;
+    for (const auto& kv : g_shapes) n += kv.first.slot == g_slot ? 1 : 0;
+    return n;
 }
 
 // Keeps a shape's plans and slot maps alive for a scope (CP-ALS graphs).
