@@ -549,7 +549,13 @@ static ModePlan plan_view(long long L, long long I, long long R, int C, int kind
         const char* e = std::getenv("DMTK_GPU_MAX_STAGES");
         return e ? std::max(2, std::min(6, std::atoi(e))) : 6;
     }();
-    for (int st = max_stages; st >= 2; --st) {
+    // A builder warp's consecutive items lie tc_builders / G stages apart, and
+    // it waits for its slot by mbarrier phase PARITY: the ring must be at
+    // least that deep, or a builder can pass a wait two phases early (it then
+    // writes a B tile into a slot still being read; 2-stage rings at G = 1 hung
+    // or faulted with more than one tile per CTA).
+    const int min_stages = std::max(2, (tc_builders(p.RB) + p.G - 1) / p.G);
+    for (int st = std::max(max_stages, min_stages); st >= min_stages; --st) {
         const int sm = tc_smem_bytes(mp.nb, mp.tail, p.G, st, p.RB);
         if (sm > 0 && sm <= 227 * 1024) {
             p.stages = st;

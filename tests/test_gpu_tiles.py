@@ -264,3 +264,19 @@ def test_shape_cache_is_bounded(oracle):
     assert np.array_equal(dg.mttkrp(dg.MttkrpRequest(t, f, 1)).m, want)
     t.release()
 
+
+
+@pytest.mark.parametrize("g", ["1", "2"])
+def test_shallow_ring_requests(g):
+    """A ring depth request below what the builders' parity waits need
+    (DMTK_GPU_MAX_STAGES=2 at one row group: a builder's consecutive items lie
+    three stages apart) is deepened to 3 stages; two row groups run a 2-stage
+    ring. Multi-tile shapes (CTAs crossing tile boundaries), every mode and
+    algorithm against an einsum reference (tools/check_shapes.py) -- the 2-stage
+    ring at G = 1 used to hang or fault."""
+    env = dict(os.environ, DMTK_GPU_MAX_STAGES="2", DMTK_GPU_FORCE_G=g)
+    shapes = ["1000x100x50:16", "700x60x40:25", "300x20x30x12:20"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
