@@ -669,6 +669,89 @@ __global__ void __launch_bounds__(256) als_solve_kernel(const double* __restrict
 // factorisation takes its square root of, so the same 1e-12 * trace test
 // sends singular systems to the Jacobi fallback (flag 0). Entries are
 // double-buffered in shared memory (one barrier per step).
+// Pseudo-inverse by cyclic Jacobi (linalg.cpp:281-326, 358-386) inside the
+// calling CTA, n <= 32: H from global memory, a and v in shared memory (row
+// pitch LDA), Hinv = V diag(gain) V^T written to global memory. The ALS
+// solve's fallback for a singular H (same sweep, stop and clip rules as
+// jacobi_kernel), so the update chain needs no separate Jacobi launches.
+template <int LDA>
+__device__ void jacobi_pinv_cta(const double* __restrict__ H, int n, double* a, double* v, double* gain,
+                                double* __restrict__ Hinv) {
+    __shared__ double s_cs, s_sn;
+    __shared__ int s_done;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - (e / n) * n;
+        a[i * LDA + j] = H[e];
+        v[i * LDA + j] = i == j ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int sweep = 0; sweep < 128; ++sweep) {
+        if (tid == 0) {
+            double off = 0.0, diag = 0.0;
+            for (int p = 0; p < n; ++p)
+                for (int q = p + 1; q < n; ++q) off += a[p * LDA + q] * a[p * LDA + q];
+            for (int p = 0; p < n; ++p) diag += a[p * LDA + p] * a[p * LDA + p];
+            s_done = (off <= 1e-300) || (off <= 1e-30 * (diag > 1e-300 ? diag : 1e-300));
+        }
+        __syncthreads();
+        if (s_done) break;
+        for (int p = 0; p < n; ++p) {
+            for (int q = p + 1; q < n; ++q) {
+                if (tid == 0) {
+                    const double apq = a[p * LDA + q];
+                    if (apq == 0.0) {
+                        s_cs = 1.0;
+                        s_sn = 0.0;
+                    } else {
+                        const double theta = (a[q * LDA + q] - a[p * LDA + p]) / (2.0 * apq);
+                        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        s_cs = 1.0 / sqrt(t * t + 1.0);
+                        s_sn = t * s_cs;
+                    }
+                }
+                __syncthreads();
+                const double cs = s_cs, sn = s_sn;
+                if (sn != 0.0 || cs != 1.0) {
+                    for (int r = tid; r < n; r += blockDim.x) {
+                        const double arp = a[r * LDA + p], arq = a[r * LDA + q];
+                        a[r * LDA + p] = cs * arp - sn * arq;
+                        a[r * LDA + q] = sn * arp + cs * arq;
+                    }
+                    __syncthreads();
+                    for (int c = tid; c < n; c += blockDim.x) {
+                        const double apc = a[p * LDA + c], aqc = a[q * LDA + c];
+                        a[p * LDA + c] = cs * apc - sn * aqc;
+                        a[q * LDA + c] = sn * apc + cs * aqc;
+                    }
+                    for (int r = tid; r < n; r += blockDim.x) {
+                        const double vrp = v[r * LDA + p], vrq = v[r * LDA + q];
+                        v[r * LDA + p] = cs * vrp - sn * vrq;
+                        v[r * LDA + q] = sn * vrp + cs * vrq;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (tid == 0) {
+        double lam_max = 0.0;
+        for (int i = 0; i < n; ++i) lam_max = a[i * LDA + i] > lam_max ? a[i * LDA + i] : lam_max;
+        const double fl = 1e-12 * lam_max;
+        for (int i = 0; i < n; ++i) {
+            const double lam = a[i * LDA + i];
+            gain[i] = (lam > fl && lam > 0.0) ? 1.0 / lam : 0.0;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - (e / n) * n;
+        double t = 0.0;
+        for (int k = 0; k < n; ++k) t = fma(v[i * LDA + k] * gain[k], v[j * LDA + k], t);
+        Hinv[e] = t;
+    }
+}
+
 __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restrict__ grams, int nmodes, int skip,
                                                            int n, double* __restrict__ Hout,
                                                            double* __restrict__ Hinv, int* __restrict__ flag) {
@@ -702,7 +785,12 @@ __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restr
         double* b = A[(k + 1) & 1];
         const double p = a[k * LDA + k];
         if (p <= tol) {  // uniform across the CTA: every thread reads the same pivot
-            if (tid == 0) flag[0] = 0;
+            // singular H: the Jacobi pseudo-inverse (solve_psd's fallback) in
+            // this CTA, applied by the same apply_inverse launch
+            __shared__ double s_gain[32];
+            __syncthreads();  // every thread has read the pivot before A is reused
+            jacobi_pinv_cta<LDA>(Hout, n, A[0], A[1], s_gain, Hinv);
+            if (tid == 0) flag[0] = 1;
             return;
         }
         const double r = 1.0 / p;
@@ -1295,20 +1383,26 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         double* V = scratch + 64 * 64;
         double* gain = V + 64 * 64;
         static const bool chol = std::getenv("DMTK_GPU_ALS_CHOL_INVERSE") != nullptr;
+        // the Gauss-Jordan CTA handles a singular H itself (Jacobi pseudo-
+        // inverse into Hinv): solve + apply, no fallback launches
+        const long long tot = rows * C;
         if (chol)
             launch_pdl(als_solve_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
         else
             launch_pdl(als_solve_gj_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
-        const long long tot = rows * C;
-        launch_pdl(apply_inverse_kernel, dim3(static_cast<unsigned>((tot + 255) / 256)), dim3(256), C * C * 8, s, Hinv, C, M, rows, U,
-                                                                                            flag);
-        launch_pdl(jacobi_kernel, dim3(1), dim3(64), 0, s, H, C, V, gain, flag);
-        const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
-        launch_pdl(jacobi_apply_rows_kernel, dim3(gb), dim3(128), 0, s, V, gain, C, M, rows, U, flag);
-        if (solve_only) return 4;
+        launch_pdl(apply_inverse_kernel, dim3(static_cast<unsigned>((tot + 255) / 256)), dim3(256), C * C * 8, s, Hinv, C,
+                   M, rows, U, flag);
+        int nl = 2;
+        if (chol) {  // the Cholesky route keeps the separate fallback
+            launch_pdl(jacobi_kernel, dim3(1), dim3(64), 0, s, H, C, V, gain, flag);
+            const unsigned gb = static_cast<unsigned>((rows + 127) / 128);
+            launch_pdl(jacobi_apply_rows_kernel, dim3(gb), dim3(128), 0, s, V, gain, C, M, rows, U, flag);
+            nl += 2;
+        }
+        if (solve_only) return nl;
         launch_normalize_cols(U, rows, C, lambda, s);
         launch_gram(U, rows, C, Gn, s);
-        return 6;
+        return nl + 2;
     }
     launch_hadamard_grams(grams, nmodes, C, skip, H, s);
     if (exact)

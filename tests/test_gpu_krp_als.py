@@ -289,3 +289,20 @@ def test_loopback_sharded_rank_above_64(oracle, ref):
     res, _ = loopback_cp_als(t, 3, AlsConfig(rank=rank, max_iters=4, tol=0.0, seed=2))
     want = ref.cp_als(x, dims, rank, 4, tol=0.0, seed=2)
     assert np.max(np.abs(np.array(res[0].fits) - want["fits"])) <= 1e-9
+
+
+@pytest.mark.parametrize("dims,rank,tree", [((2, 2, 2), 5, False), ((3, 2, 4), 7, False), ((2, 3, 2, 2), 6, False),
+                                            ((2, 3, 2, 2), 6, True)])
+def test_cp_als_singular_systems_match_reference(ref, oracle, dims, rank, tree):
+    """Ranks above what the tiny extents support make every H = Hadamard of
+    Grams singular (a 2-row factor's Gram has rank 2): each ALS update takes
+    the Jacobi pseudo-inverse, which the Gauss-Jordan solve CTA now computes
+    itself (no separate fallback launches). Such ranks exceed the tensor's
+    rank; near an exact fit, fit = 1 - sqrt(res^2) / ||X|| turns
+    rounding-level differences of res^2 (~1e-16) into ~1e-8, so the bound on
+    the fits is 1e-7."""
+    x = oracle.gen_tensor(dims, 5)
+    res = cp(x, dims, rank, 6, 11, tree=tree)
+    got = np.array([it.fit.fit for it in res.trace.iters])
+    rf = ref.cp_als(x, dims, rank, 6, tol=0.0, seed=11)
+    assert np.max(np.abs(got - rf["fits"])) <= 1e-7, (got, rf["fits"])
