@@ -409,3 +409,35 @@ def test_slab_is_its_own_extent(oracle, dims, C):
             assert np.linalg.norm(got[:rows * C].reshape(rows, C) - want) <= 1e-12 * np.linalg.norm(want)
         s.release()
         own.release()
+
+
+@pytest.mark.parametrize("exchange", ["xrank", "nccl"])
+def test_device_mttkrp_sharded_world1(group, oracle, exchange):
+    """bench.py's N > 1 MTTKRP path (dmtk_gpu_mttkrp_sharded through a
+    library-owned NCCL communicator) at world 1: the fused exchange kernel's
+    real one-rank launch, or the NCCL all-reduce; equal to the single-device
+    MTTKRP (1e-12) for every mode, twice in a row."""
+    import paper_1708_08976_b200 as dg
+    from paper_1708_08976_b200.distributed import DeviceComm
+    dims, C = (60, 40, 30), 12
+    x = oracle.gen_tensor(dims, 3)
+    f = oracle.gen_factors(dims, C, 4)
+    t = dg.DenseTensor(dims, x)
+    if exchange == "nccl":
+        os.environ["DMTK_GPU_XRANK"] = "0"
+    try:
+        comm = DeviceComm(0)
+    finally:
+        os.environ.pop("DMTK_GPU_XRANK", None)
+    assert comm.fused == (exchange == "xrank")
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in f]
+    s = torch.cuda.Stream()
+    for _ in range(2):
+        for m in range(3):
+            out = torch.zeros((dims[m], C), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            comm.mttkrp(t, [a.data_ptr() for a in dev], C, m, out.data_ptr(), s.cuda_stream)
+            torch.cuda.synchronize()
+            want = dg.mttkrp(dg.MttkrpRequest(t, f, m)).m
+            assert np.linalg.norm(out.cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want)
+    comm.close()
