@@ -37,10 +37,7 @@ constexpr int kConsumerWarps = 8;  // two per SM sub-partition
 // Tile shape by RB (DMMA row blocks per consumer warp, 2..4): tile rows
 // 64 * RB at G = 1; contraction indices per stage (and row group) 32 for
 // RB = 2, 16 for taller tiles, so a stage stays 24-32 KB of X.
-#ifndef DMTK_BK_TALL
-#define DMTK_BK_TALL 16
-#endif
-__host__ __device__ constexpr int tc_bk(int rb) { return rb == 2 ? 32 : DMTK_BK_TALL; }
+__host__ __device__ constexpr int tc_bk(int rb) { return rb == 2 ? 32 : 16; }
 __host__ __device__ constexpr int tc_bm(int rb) { return kConsumerWarps * 8 * rb; }
 // Warp roles: producer, three builders, eight consumers (see mttkrp_tc.cuh).
 // (A setmaxnreg rebalance toward the consumers was measured to add spills,
