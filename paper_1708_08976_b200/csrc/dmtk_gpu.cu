@@ -2874,57 +2874,83 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         steps.push_back({fit_step, -1});
         const int NS = static_cast<int>(steps.size());  // the last one is the fit
         // Iteration 1 runs eagerly (it builds every plan, CSR map and buffer);
-        // the later ones replay one CUDA graph per step of the same launches.
-        std::vector<cudaGraphExec_t> gexec(static_cast<size_t>(NS), nullptr);
-        std::vector<long long> gkernels(static_cast<size_t>(NS), 0);
+        // the later ones replay ONE CUDA graph of the whole iteration (no gaps
+        // between the steps' launches). Per-step timing: event-record nodes
+        // whose events are re-pointed at the iteration's own events before
+        // each launch; the fit history is appended on the device.
+        cudaGraph_t gtmpl = nullptr;
+        cudaGraphExec_t gexec = nullptr;
+        long long gkernels = 0;
+        std::vector<cudaGraphNode_t> ev_nodes(static_cast<size_t>(NS), nullptr);
         bool graphs = false;
         std::vector<cudaEvent_t> evs(static_cast<size_t>(std::max(iters, 1)) * NS);
         for (auto& e : evs) CK(cudaEventCreate(&e));
+        std::vector<cudaEvent_t> cev(static_cast<size_t>(NS));  // capture placeholders
+        for (auto& e : cev) CK(cudaEventCreate(&e));
+        DevBuf hist;  // (an int counter)
+        hist.ensure(1);
+        int* hist_count = reinterpret_cast<int*>(hist.p);
         std::vector<double> f4(4 * fit_slots, 0.0);
         double prev_fit = 0.0;
         int done = 0;
-        for (int iter = 1; iter <= iters; ++iter) {
-            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * NS;
+        auto run_steps = [&](cudaEvent_t* ev) {
             for (int st = 0; st < NS; ++st) {
                 if (st < NS - 1) CK(cudaEventRecord(ev[st], s));
-                if (graphs) {
-                    CK(cudaGraphLaunch(gexec[st], s));
-                    count_launch(static_cast<int>(gkernels[st]));
-                } else {
-                    steps[st].fn();
-                }
+                steps[st].fn();
                 if (st == NS - 2) CK(cudaEventRecord(ev[NS - 1], s));
             }
-            CK(cudaMemcpyAsync(fitb + 4 * iter, fitb, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        };
+        for (int iter = 1; iter <= iters; ++iter) {
+            cudaEvent_t* ev = evs.data() + static_cast<size_t>(iter - 1) * NS;
+            if (graphs) {
+                for (int k = 0; k < NS; ++k) CK(cudaGraphExecEventRecordNodeSetEvent(gexec, ev_nodes[k], ev[k]));
+                CK(cudaGraphLaunch(gexec, s));
+                count_launch(static_cast<int>(gkernels));
+            } else {
+                run_steps(ev);
+                CK(cudaMemcpyAsync(fitb + 4 * iter, fitb, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            }
             if (iter == 1 && iters > 1 && !(sh && sh->loop)) {  // capture after the eager warm-up iteration
-                bool ok = true;
-                for (int st = 0; st < NS && ok; ++st) {
-                    cudaGraph_t g = nullptr;
-                    const long long before = g_launches.load();
-                    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-                        ok = false;
-                        break;
-                    }
+                const int one = 1;
+                CK(cudaMemcpyAsync(hist_count, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+                bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                const long long before = g_launches.load();
+                if (ok) {
                     try {
-                        steps[st].fn();
+                        run_steps(cev.data());
+                        launch_fit_history(fitb, hist_count, s);
+                        check_launch("fit_history");
                     } catch (const Err&) {
                         ok = false;
                     }
-                    const cudaError_t ec = cudaStreamEndCapture(s, &g);
-                    if (!ok || ec != cudaSuccess || !g || cudaGraphInstantiate(&gexec[st], g, 0) != cudaSuccess)
+                    const cudaError_t ec = cudaStreamEndCapture(s, &gtmpl);
+                    if (!ok || ec != cudaSuccess || !gtmpl || cudaGraphInstantiate(&gexec, gtmpl, 0) != cudaSuccess)
                         ok = false;
-                    if (g) cudaGraphDestroy(g);
-                    gkernels[st] = g_launches.load() - before;
-                    g_launches.fetch_sub(gkernels[st]);  // captured, not launched
+                }
+                gkernels = g_launches.load() - before;
+                g_launches.fetch_sub(gkernels);  // captured, not launched
+                if (ok) {  // the event-record node of each capture placeholder
+                    size_t nn = 0;
+                    ok = cudaGraphGetNodes(gtmpl, nullptr, &nn) == cudaSuccess;
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    if (ok && nn) ok = cudaGraphGetNodes(gtmpl, nodes.data(), &nn) == cudaSuccess;
+                    for (size_t q = 0; ok && q < nn; ++q) {
+                        cudaGraphNodeType ty;
+                        if (cudaGraphNodeGetType(nodes[q], &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord)
+                            continue;
+                        cudaEvent_t e = nullptr;
+                        if (cudaGraphEventRecordNodeGetEvent(nodes[q], &e) != cudaSuccess) continue;
+                        for (int k = 0; k < NS; ++k)
+                            if (cev[k] == e) ev_nodes[k] = nodes[q];
+                    }
+                    for (int k = 0; k < NS; ++k) ok = ok && ev_nodes[k] != nullptr;
                 }
                 cudaGetLastError();
                 graphs = ok;
-                if (!ok)
-                    for (auto& ge : gexec)
-                        if (ge) {
-                            cudaGraphExecDestroy(ge);
-                            ge = nullptr;
-                        }
+                if (!ok && gexec) {
+                    cudaGraphExecDestroy(gexec);
+                    gexec = nullptr;
+                }
             }
             done = iter;
             if (cfg->tol > 0.0) {  // the stopping rule needs this iteration's fit on the host
@@ -2952,9 +2978,10 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         }
         if (start && start->fit4_out && done > 0)
             for (int k = 0; k < 4; ++k) start->fit4_out[k] = f4[4 * done + k];
-        for (auto& ge : gexec)
-            if (ge) cudaGraphExecDestroy(ge);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (gtmpl) cudaGraphDestroy(gtmpl);
         for (auto& e : evs) cudaEventDestroy(e);
+        for (auto& e : cev) cudaEventDestroy(e);
         {
             long long lo_ = 0, po = 0;  // logical rows only
             for (int k = 0; k < N; ++k) {

@@ -367,6 +367,18 @@ __global__ void fill_kernel(double* p, long long n, double v) {
         p[e] = v;
 }
 
+// CP-ALS fit history inside the iteration graph: slot 0 (this iteration's
+// fit record) appended at slot (++*count), the counter living on the device so
+// every replay of the same graph writes the next slot.
+__global__ void fit_history_kernel(double* fitb, int* count) {
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        const int k = ++count[0];
+        for (int q = 0; q < 4; ++q) fitb[4 * k + q] = fitb[q];
+    }
+}
+
 // Cholesky with pivot floor 1e-12 * trace (linalg.cpp:254-276), one CTA.
 // Writes L (row-major, lower) and flag[0] = 1 on success, 0 on failure.
 __global__ void cholesky_kernel(const double* __restrict__ H, int n, double* __restrict__ Lm, int* __restrict__ flag) {
@@ -1289,6 +1301,10 @@ void launch_matricize(const double* X, long long L, long long I, long long R, do
 
 void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s) {
     launch_pdl(gram_hadamard_accum_kernel, dim3((C * C + 127) / 128), dim3(128), 0, s, U, rows, C, H, first ? 1 : 0);
+}
+
+void launch_fit_history(double* fitb, int* count, cudaStream_t s) {
+    launch_pdl(fit_history_kernel, dim3(1), dim3(32), 0, s, fitb, count);
 }
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {

@@ -80,6 +80,7 @@ void launch_slot_reduce(const double* ws, const long long* rowptr, const long lo
 void launch_matricize(const double* X, long long L, long long I, long long R, double* dst, cudaStream_t s);
 void launch_gram_hadamard_accum(const double* U, long long rows, int C, double* H, bool first, cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);
+void launch_fit_history(double* fitb, int* count, cudaStream_t s);
 // scratch: >= 2*64*64 + 64 doubles; flag: 1 int
 // Same contract through H^-1 = L^-T L^-1 and one dot product per output
 // element (the ALS loop's fast path; rounding differs from the substitution).
