@@ -119,7 +119,10 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             p.trace[static_cast<long long>(blockIdx.x) * kTraceSlots + ev] = gt;
         }
     };
-    if (threadIdx.x == 0) stamp(kTrEntry);
+    if (threadIdx.x == 0) {
+        stamp(kTrEntry);
+        if (p.trace) p.trace[static_cast<long long>(blockIdx.x) * kTraceSlots + kTrClkEntry] = clock64();
+    }
     // shared-window addresses, computed once (no per-stage address conversion)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), sA_a = smem_u32(sA);
     long long lo, hi;
@@ -928,7 +931,10 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         }
         if (lane == 0 && w == 0) stamp(kTrConsEpi);
     }
-    if (lane == 0 && w == 0) stamp(kTrExit);
+    if (lane == 0 && w == 0) {
+        stamp(kTrExit);
+        if (p.trace) p.trace[static_cast<long long>(blockIdx.x) * kTraceSlots + kTrClkExit] = clock64();
+    }
 }
 
 }  // namespace dmtkg

@@ -2,8 +2,8 @@
 # (developer tool):  bash tools/exp_lib_ab.sh <libA> <libB> <configs> [rounds]
 A=$1; B=$2; CFG=$3; R=${4:-3}
 for i in $(seq 1 $R); do
-  DMTK_GPU_LIB=$A python tools/perf_modes.py --config $CFG --reps 10 > gpurun_out/ab_A_$i.log 2>&1
-  DMTK_GPU_LIB=$B python tools/perf_modes.py --config $CFG --reps 10 > gpurun_out/ab_B_$i.log 2>&1
+  DMTK_GPU_LIB=$A python tools/perf_modes.py --config $CFG --reps ${REPS:-10} > gpurun_out/ab_A_$i.log 2>&1
+  DMTK_GPU_LIB=$B python tools/perf_modes.py --config $CFG --reps ${REPS:-10} > gpurun_out/ab_B_$i.log 2>&1
 done
 python - "$R" <<'PY'
 import json, collections, sys

@@ -28,6 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="200c16")
     ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--warm", type=int, default=1, help="untraced calls per mode before the traced one")
     a = ap.parse_args()
     dims, Cr = CONFIGS[a.config]
     n = 1
@@ -44,7 +45,8 @@ def main():
         out = torch.empty((dims[mode], Cr), dtype=torch.float64, device="cuda")
         call = lambda: dg.mttkrp_device(t, [f.data_ptr() for f in fs], Cr, mode, A.automatic, O.automatic,
                                         out.data_ptr(), s.cuda_stream)
-        call()
+        for _ in range(a.warm):
+            call()
         torch.cuda.synchronize()
         if junk is not None:
             junk.fill_(1.0)
@@ -57,6 +59,10 @@ def main():
         ent = [(r[0] - t0) / 1e3 for r in rows]
         print(f"mode {mode}: {nct.value} CTAs; entry spread us min/med/max "
               f"{min(ent):.2f}/{statistics.median(ent):.2f}/{max(ent):.2f}")
+        ghz = [(r[12] - r[11]) / (r[10] - r[0]) for r in rows if r[10] > r[0] and r[12] > r[11]]
+        if ghz:
+            print(f"  SM clock GHz (clock64 / globaltimer, entry to exit): median {statistics.median(ghz):.3f} "
+                  f"min {min(ghz):.3f} max {max(ghz):.3f}")
         for ev in range(1, len(EVENTS)):
             v = [(r[ev] - r[0]) / 1e3 for r in rows if r[ev]]
             if v:
