@@ -98,6 +98,29 @@ static long long prod(const std::vector<long long>& d, int a, int b) {  // prod 
 }
 
 // --------------------------------------------------------- device buffers
+// cudaMalloc with the request and the device's free memory in the error text
+static void dev_alloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 8));
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) {
+        // the stream-ordered pool keeps every freed tensor buffer (release
+        // threshold: everything): give its idle blocks back and retry once
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+            cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess && cudaMemPoolTrimTo(pool, 0) == cudaSuccess) {
+            e = cudaMalloc(p, std::max<size_t>(bytes, 8));
+            if (e == cudaSuccess) return;
+        }
+        cudaGetLastError();
+    }
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    fail(DMTK_GPU_ERUNTIME, "CUDA error in cudaMalloc of " + std::to_string(bytes) + " bytes (" + std::to_string(fr) +
+                                " of " + std::to_string(tot) + " free): " + cudaGetErrorString(e));
+}
+
 struct DevBuf {
     double* p = nullptr;
     size_t n = 0;  // doubles
@@ -106,7 +129,7 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
-        CK(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(double)));
+        dev_alloc(reinterpret_cast<void**>(&p), want * sizeof(double));
         n = want;
     }
     ~DevBuf() {
@@ -122,7 +145,7 @@ struct DevBufLL {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
-        CK(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(long long)));
+        dev_alloc(reinterpret_cast<void**>(&p), want * sizeof(long long));
         n = want;
     }
     ~DevBufLL() {

@@ -26,3 +26,19 @@ def ref():
     if not os.path.exists(REF_SO):
         pytest.skip("oracle/_ref not built (reference sources absent)")
     return Ref()
+
+
+def pytest_runtest_teardown(item, nextitem):
+    # developer aid: DMTK_TEST_MEMLOG=<file> appends the device's free memory after every test
+    path = os.environ.get("DMTK_TEST_MEMLOG")
+    if not path:
+        return
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+        free, total = torch.cuda.mem_get_info()
+        with open(path, "a") as f:
+            f.write(f"{free / 2**30:8.2f} GiB free  torch_reserved {torch.cuda.memory_reserved() / 2**30:7.2f}  {item.nodeid}\n")
+    except Exception:  # never fail a test over the log
+        pass

@@ -103,11 +103,14 @@ def fmri_tensor(dims, seed=1):
     n0, n1 = dims[0], dims[1]
     rest = tuple(dims[2:])[::-1]
     g = torch.Generator(device="cuda").manual_seed(seed)
-    z = torch.tanh(torch.randn(rest + (n1, n0), dtype=torch.float64, device="cuda", generator=g) * 0.3)
-    z = torch.triu(z, diagonal=1)
-    z = z + z.transpose(-1, -2)
+    # in place (two 7.7 GB buffers at the peak, not five)
+    torch.cuda.empty_cache()
+    z = torch.randn(rest + (n1, n0), dtype=torch.float64, device="cuda", generator=g)
+    z.mul_(0.3).tanh_().triu_(diagonal=1)
+    z.add_(z.transpose(-1, -2).contiguous())
     z.diagonal(dim1=-2, dim2=-1).fill_(1.0)
-    return z.reshape(-1).contiguous()
+    torch.cuda.empty_cache()
+    return z.reshape(-1)
 
 
 def test_cp_als_fmri_full_size_sweeps_agree():
