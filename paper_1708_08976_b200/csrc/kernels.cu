@@ -259,62 +259,83 @@ __global__ void mttkrp_generic_kernel(const double* __restrict__ X, long long L,
 
 // ------------------------------------------------------------ CSR reduce
 // out(i, c) = sum_{e in [rowptr[i], rowptr[i+1])} ws(slot[e], c), fixed order.
-// One CTA per output row: thread (p, c) sums slots k = p + P (4 j + q) of the
-// row's CSR range for column c (coalesced over c) in four independent chains
-// q (a serial FP64 add chain costs ~100 cycles per link on B200, and each
-// link waits on two dependent loads), the chains and then the P partials
-// added in a fixed order: deterministic, with 4 P load streams per row.
+// One CTA per output row: thread (p, c) sums slots k = p + P m (m = 0, 1, ...)
+// of the row's CSR range for column c (coalesced over c) in four independent
+// chains m & 3 (a serial FP64 add chain costs ~100 cycles per link on B200),
+// the chains and then the P partials added in a fixed order: deterministic.
+// The CSR map is static (written at plan time, before the streaming kernel
+// was launched), so its two dependent loads (row range, slot ids) are issued
+// BEFORE the programmatic-launch wait and overlap the streaming kernel's
+// tail; after the wait one round of independent slot loads remains.
 constexpr int kReduceThreads = 256;
+constexpr int kReduceBatch = 8;  // slot ids a thread holds in registers per round
 __global__ void __launch_bounds__(kReduceThreads) slot_reduce_kernel(const double* __restrict__ ws,
                                                                      const long long* __restrict__ rowptr,
                                                                      const long long* __restrict__ slots, int C,
                                                                      double* __restrict__ out) {
     __shared__ double part[kReduceThreads];
-    pdl_wait();  // the slots are the streaming kernel's output
-    pdl_trigger();
     const long long i = blockIdx.x;
     const int P = kReduceThreads / C;
     const int p = threadIdx.x / C;
     const int c = threadIdx.x - p * C;
-    const long long k0 = rowptr[i], k1 = rowptr[i + 1];
+    const long long k0 = __ldg(rowptr + i), k1 = __ldg(rowptr + i + 1);
+    long long k = k0 + p;
+    long long e[kReduceBatch];
+#pragma unroll
+    for (int m = 0; m < kReduceBatch; ++m) e[m] = (p < P && k + m * P < k1) ? __ldg(slots + k + m * P) : -1;
+    pdl_wait();  // the slots are the streaming kernel's output
+    pdl_trigger();
     double s = 0.0;
     if (p < P) {
         double q[4] = {0.0, 0.0, 0.0, 0.0};
-        long long k = k0 + p;
-        for (; k + 3 * P < k1; k += 4 * P) {
-            const long long e0 = slots[k], e1 = slots[k + P], e2 = slots[k + 2 * P], e3 = slots[k + 3 * P];
-            q[0] += ws[e0 * C + c];
-            q[1] += ws[e1 * C + c];
-            q[2] += ws[e2 * C + c];
-            q[3] += ws[e3 * C + c];
+        for (;;) {
+            double v[kReduceBatch];
+#pragma unroll
+            for (int m = 0; m < kReduceBatch; ++m) v[m] = e[m] >= 0 ? ws[e[m] * C + c] : 0.0;
+#pragma unroll
+            for (int m = 0; m < kReduceBatch; ++m)
+                if (e[m] >= 0) q[m & 3] += v[m];
+            k += static_cast<long long>(kReduceBatch) * P;
+            if (k >= k1) break;  // (rows with more than 8 P slots: further rounds)
+#pragma unroll
+            for (int m = 0; m < kReduceBatch; ++m) e[m] = k + m * P < k1 ? __ldg(slots + k + m * P) : -1;
         }
-        if (k < k1) q[0] += ws[slots[k] * C + c];  // at most three left
-        if (k + P < k1) q[1] += ws[slots[k + P] * C + c];
-        if (k + 2 * P < k1) q[2] += ws[slots[k + 2 * P] * C + c];
         s = (q[0] + q[1]) + (q[2] + q[3]);
     }
     part[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x < C) {
-        double t = 0.0;
-        for (int r = 0; r < P; ++r) t += part[r * C + threadIdx.x];
-        out[i * C + threadIdx.x] = t;
+        double u[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int r = 0; r < P; ++r) u[r & 3] += part[r * C + threadIdx.x];
+        out[i * C + threadIdx.x] = (u[0] + u[1]) + (u[2] + u[3]);
     }
 }
 
 // Thin variant for maps with a few slots per row (K-major views with many
-// output rows): one thread per (row, column), the row's slots in CSR order.
+// output rows): one thread per (row, column), the row's slots in CSR order
+// (slot ids loaded before the wait, slot values in independent loads).
 __global__ void slot_reduce_thin_kernel(const double* __restrict__ ws, const long long* __restrict__ rowptr,
                                         const long long* __restrict__ slots, long long rows, int C,
                                         double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = e < rows * C;
+    const long long i = live ? e / C : 0;
+    const int c = static_cast<int>(e - i * C);
+    const long long k0 = live ? __ldg(rowptr + i) : 0, k1 = live ? __ldg(rowptr + i + 1) : 0;
+    long long id[kReduceBatch];
+#pragma unroll
+    for (int m = 0; m < kReduceBatch; ++m) id[m] = k0 + m < k1 ? __ldg(slots + k0 + m) : -1;
     pdl_wait();
     pdl_trigger();
-    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= rows * C) return;
-    const long long i = e / C;
-    const int c = static_cast<int>(e - i * C);
+    if (!live) return;
+    double v[kReduceBatch];
+#pragma unroll
+    for (int m = 0; m < kReduceBatch; ++m) v[m] = id[m] >= 0 ? ws[id[m] * C + c] : 0.0;
     double t = 0.0;
-    for (long long k = rowptr[i]; k < rowptr[i + 1]; ++k) t += ws[slots[k] * C + c];
+#pragma unroll
+    for (int m = 0; m < kReduceBatch; ++m)
+        if (id[m] >= 0) t += v[m];
+    for (long long k = k0 + kReduceBatch; k < k1; ++k) t += ws[__ldg(slots + k) * C + c];
     out[e] = t;
 }
 

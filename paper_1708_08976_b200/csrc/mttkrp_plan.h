@@ -94,6 +94,8 @@ enum TraceEv : int {
     kTrEntry = 0, kTrPrologue = 1, kTrTmaFirst = 2, kTrTmaLast = 3, kTrBuildFirst = 4, kTrBuildLast = 5,
     kTrConsFirst = 6, kTrConsLoop = 7, kTrConsEpi = 8, kTrCons7Loop = 9, kTrExit = 10,
     kTrClkEntry = 11, kTrClkExit = 12,  // clock64 (SM cycles) at entry and exit: the SM clock rate
+    kTrBuildStart = 13,                   // builder warp 0 enters its item loop
+    kTrBuildLoaded = 14,                  // ... has issued its first item's factor / head loads
     kTrStageIssue = 16,                   // producer: stage k's loads issued
     kTrStageReady = 16 + kTraceStages,    // observer: stage k's full barrier complete
 };

@@ -203,6 +203,51 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
             }
         }
     }
+    // Meanwhile the other warps stage the builders' small fastest factor in
+    // shared memory (u0_pitch > 0), one batch of independent loads per
+    // thread, and the builders pull the first head-table rows toward L1: the
+    // first B tile is then an LDS + multiply away once the barriers are up,
+    // instead of two more dependent global round trips after the CTA barrier.
+    // (Factor rows may be the previous kernel's output: pdl_wait first.)
+    if (warp != kProducerWarp && !(p.debug & 1)) {
+        const KrpGen& Gen = p.bgen;
+        const int C = p.C;
+        if (p.u0_pitch > 0) {
+            pdl_wait();
+            const int P = p.u0_pitch;
+            const int n = static_cast<int>(Gen.ext[0]) * C;
+            const double* __restrict__ U0 = Gen.U[0];
+            const long long ldu = Gen.ldu;
+            constexpr int kStageThreads = tc_threads(RB) - 32;
+            constexpr int kBatch = 8;
+            for (int base = threadIdx.x - 32; base < n; base += kStageThreads * kBatch) {
+                double v[kBatch];
+                int so[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int e = base + u * kStageThreads;
+                    const int r = static_cast<int>(static_cast<unsigned>(e < n ? e : 0) / static_cast<unsigned>(C));
+                    const int cc = (e < n ? e : 0) - r * C;
+                    so[u] = e < n ? r * P + cc : -1;
+                    v[u] = e < n ? __ldg(U0 + static_cast<long long>(r) * ldu + cc) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+                    if (so[u] >= 0) sU0[so[u]] = v[u];
+            }
+        }
+        if (warp < kFirstConsumerWarp && p.htab && Gen.ext[0] >= BK && lo < hi) {
+            pdl_wait();
+            const long long st0 = lo - div_nn(lo, spt) * spt;
+            const long long kb0 =
+                (KMAJ && p.flavor == kKMajorJK ? st0 - div_nn(st0, p.n_lc) * p.n_lc : st0) * BK * G;
+            const long long q0 = div_nn(kb0, Gen.ext[0]);
+            const long long nrow = p.hrows - q0 < 4 ? p.hrows - q0 : 4;  // the first ring fill's head rows
+            const char* hb = reinterpret_cast<const char*>(p.htab + q0 * C);
+            for (long long off = (threadIdx.x - kFirstBuilderWarp * 32) * 128LL; off < nrow * C * 8; off += kBuilderWarps * 32 * 128LL)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(hb + off));
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) stamp(kTrPrologue);
     // Programmatic dependent launch: the producer streams X (never written by
@@ -346,20 +391,14 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
         const double* __restrict__ U0 = Gen.U[0];
         const long long ldu = Gen.ldu;
         const int P = p.u0_pitch;  // > 0: U0 staged in shared memory with this row pitch
-        if (P > 0) {
-            const int n = static_cast<int>(e0) * C;
-            for (int e = threadIdx.x - kFirstBuilderWarp * 32; e < n; e += kBuilderWarps * 32) {
-                const int r = e / C;
-                sU0[r * P + (e - r * C)] = U0[static_cast<long long>(r) * ldu + (e - r * C)];
-            }
-            named_bar_sync(1, kBuilderWarps * 32);
-        }
+        // (P > 0: sU0 was staged by every non-producer warp before the CTA barrier)
         const uint32_t sU0a = smem_u32(sU0);
         double hv[2][NB];
         double ht[2];
         long long hq = -1, hj = -2;
         StageCursor cur;
         cur.init(lo, spt);
+        if (bw == 0 && lane == 0) stamp(kTrBuildStart);
         int owner = 0;  // builder warp owning the next item
         for (long long gs = lo; gs < hi; ++gs, cur.next(spt, STAGES)) {
             for (int gi = 0; gi < G; ++gi, owner = (owner + 1 == kBuilderWarps ? 0 : owner + 1)) {
@@ -494,7 +533,10 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                             }
                         }
                     }
-                    if (ch == 0) mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
+                    if (ch == 0) {
+                        if (bw == 0 && lane == 0 && gs == lo) stamp(kTrBuildLoaded);
+                        mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
+                    }
 #pragma unroll
                     for (int sp = 0; sp < SPC / 2; ++sp) {
                         const int s2 = ch * SPC / 2 + sp;

@@ -102,8 +102,9 @@ __global__ void __launch_bounds__(kXThreads) xrank_reduce_kernel(const XrankArgs
             part[threadIdx.x] = s;
             __syncthreads();
             if (threadIdx.x < C) {
-                double t = 0.0;
-                for (int q = 0; q < Q; ++q) t += part[q * C + threadIdx.x];
+                double u[4] = {0.0, 0.0, 0.0, 0.0};  // the same fold as slot_reduce_kernel
+                for (int q = 0; q < Q; ++q) u[q & 3] += part[q * C + threadIdx.x];
+                const double t = (u[0] + u[1]) + (u[2] + u[3]);
                 for (int k = 0; k < P; ++k) a.recv[k][mine + i * C + threadIdx.x] = t;
             }
             __syncthreads();

@@ -63,10 +63,10 @@ def main():
         if ghz:
             print(f"  SM clock GHz (clock64 / globaltimer, entry to exit): median {statistics.median(ghz):.3f} "
                   f"min {min(ghz):.3f} max {max(ghz):.3f}")
-        for ev in range(1, len(EVENTS)):
+        for ev, name in list(enumerate(EVENTS))[1:] + [(13, "build_start"), (14, "build_loaded")]:
             v = [(r[ev] - r[0]) / 1e3 for r in rows if r[ev]]
             if v:
-                print(f"  {EVENTS[ev]:12s} us  min {min(v):7.2f}  med {statistics.median(v):7.2f}  max {max(v):7.2f}"
+                print(f"  {name:12s} us  min {min(v):7.2f}  med {statistics.median(v):7.2f}  max {max(v):7.2f}"
                       f"  (n={len(v)})")
         # per stage k of a CTA: loads issued / full barrier complete (median over CTAs)
         line_i, line_r = [], []
