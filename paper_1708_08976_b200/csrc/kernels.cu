@@ -785,7 +785,7 @@ __device__ void jacobi_pinv_cta(const double* __restrict__ H, int n, double* a, 
     }
 }
 
-__global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restrict__ grams, int nmodes, int skip,
+__global__ void __launch_bounds__(1024) als_solve_gj_kernel(const double* __restrict__ grams, int nmodes, int skip,
                                                            int n, double* __restrict__ Hout,
                                                            double* __restrict__ Hinv, int* __restrict__ flag) {
     pdl_wait();
@@ -812,6 +812,11 @@ __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restr
     }
     __syncthreads();
     const double tol = 1e-12 * s_tr;
+    // launched with at least n * n threads when that fits a CTA: every entry
+    // then has its own thread (indices fixed outside the serial step loop,
+    // one round per step)
+    const bool own = nn <= static_cast<int>(blockDim.x);
+    const int oi = tid / n, oj = tid - (tid / n) * n;
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
         const double* a = A[k & 1];
@@ -828,7 +833,7 @@ __global__ void __launch_bounds__(256) als_solve_gj_kernel(const double* __restr
         }
         const double r = 1.0 / p;
         for (int e = tid; e < nn; e += blockDim.x) {
-            const int i = e / n, j = e - (e / n) * n;
+            const int i = own ? oi : e / n, j = own ? oj : e - (e / n) * n;
             double v;
             if (i == k)
                 v = j == k ? r : a[k * LDA + j] * r;
@@ -862,9 +867,21 @@ __global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, con
     const long long r = e / n;
     const int c = static_cast<int>(e - r * n);
     const double* mrow = M + r * n;
-    double t = 0.0;
-    for (int k = 0; k < n; ++k) t = fma(mrow[k], sHi[k * n + c], t);
-    U[e] = t;
+    // eight independent loads per round, four FMA chains (a dependent load +
+    // FMA per k costs an L2 round trip and ~100 cycles each), fixed fold
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < n; k0 += 8) {
+        double m[8], h[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u;
+            m[u] = k < n ? __ldg(mrow + k) : 0.0;
+            h[u] = k < n ? sHi[k * n + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u & 3] = fma(m[u], h[u], t[u & 3]);
+    }
+    U[e] = (t[0] + t[1]) + (t[2] + t[3]);
 }
 
 // Cyclic Jacobi pseudoinverse fallback (linalg.cpp:281-326, 358-386), one
@@ -1092,8 +1109,22 @@ __global__ void gram_warp_kernel(const double* __restrict__ U, long long rows, i
         ++c1;
     }
     const int c2 = c1 + e;
-    double s = 0.0;
-    for (long long r = threadIdx.x; r < rows; r += 32) s = fma(U[r * C + c1], U[r * C + c2], s);
+    // four independent chains per lane (rows r, r + 32, r + 64, r + 96 of a
+    // 128-row round), fixed fold: a single FMA chain costs ~100 cycles a link
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
+    long long r = threadIdx.x;
+    for (; r + 96 < rows; r += 128) {
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = U[(r + 32 * u) * C + c1];
+            b[u] = U[(r + 32 * u) * C + c2];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = fma(a[u], b[u], q[u]);
+    }
+    for (int u = 0; r < rows; r += 32, ++u) q[u] = fma(U[r * C + c1], U[r * C + c2], q[u]);
+    double s = (q[0] + q[1]) + (q[2] + q[3]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) {
@@ -1426,7 +1457,8 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
         if (chol)
             launch_pdl(als_solve_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
         else
-            launch_pdl(als_solve_gj_kernel, dim3(1), dim3(256), 0, s, grams, nmodes, skip, C, H, Hinv, flag);
+            launch_pdl(als_solve_gj_kernel, dim3(1), dim3(C * C <= 256 ? 256 : C * C <= 512 ? 512 : 1024), 0, s, grams,
+                       nmodes, skip, C, H, Hinv, flag);
         launch_pdl(apply_inverse_kernel, dim3(static_cast<unsigned>((tot + 255) / 256)), dim3(256), C * C * 8, s, Hinv, C,
                    M, rows, U, flag);
         int nl = 2;
