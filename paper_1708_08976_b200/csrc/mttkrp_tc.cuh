@@ -379,10 +379,21 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
     // is read from a shared-memory copy when it is small (LDS latency instead
     // of an L2 round trip per item), the head partial from the materialised
     // head table (one row, refreshed only when the slower digits carry).
+#ifdef DMTK_EXP_NO_TAIL_BUILD
+    constexpr bool kExpNoTailBuild = true;  // timing experiment: builders skip the tail columns (wrong results)
+#else
+    constexpr bool kExpNoTailBuild = false;
+#endif
     if (warp < kFirstConsumerWarp) {
         const int bw = warp - kFirstBuilderWarp;
         const int g = lane >> 2;
         const int t = lane & 3;
+        // tail columns (DFMA columns 8 NB .. 8 NB + TAIL - 1): the item's
+        // 4 KS TAIL entries are dealt over the lanes, entry x = (s 4 + t) TAIL
+        // + column to lane x % 32 -- one load, one multiply and one store per
+        // 32 entries (a DMUL costs the FP64 pipe the same with 4 lanes active
+        // as with 32, and the builders share that pipe with the DMMAs)
+        const int tg = TAIL > 0 ? lane % (TAIL > 0 ? TAIL : 1) : 0;  // this lane's tail column (32 % TAIL == 0)
         const KrpGen& Gen = p.bgen;
         const long long e0 = Gen.ext[0];
         const bool fast = e0 >= BK;
@@ -436,7 +447,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                                     for (int nb = 0; nb < NB; ++nb)
                                         hv[h][nb] = nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
-                                    if (TAIL > 0) ht[h] = (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    if (TAIL > 0) ht[h] = (8 * NB + tg < C) ? __ldg(row + 8 * NB + tg) : 0.0;
                                 }
                             } else {
                                 const long long idx = (q0 + h) * e0;
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                                     for (int nb = 0; nb < NB; ++nb)
                                         hv[h][nb] *= nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
-                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    if (TAIL > 0) ht[h] *= (8 * NB + tg < C) ? __ldg(row + 8 * NB + tg) : 0.0;
                                 }
                             }
                             if (jx >= 0) {
@@ -455,7 +466,7 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                                     for (int nb = 0; nb < NB; ++nb)
                                         hv[h][nb] *= nb * 8 + g < C ? __ldg(row + nb * 8 + g) : 0.0;
-                                    if (TAIL > 0) ht[h] *= (8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
+                                    if (TAIL > 0) ht[h] *= (8 * NB + tg < C) ? __ldg(row + 8 * NB + tg) : 0.0;
                                 }
                             }
                         }
@@ -466,6 +477,8 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                     for (int nb = 0; nb < NB; ++nb) hv[0][nb] = hv[1][nb] = 1.0;
                     ht[0] = ht[1] = 1.0;
                 }
+                // no head partial at all (one-factor B rows, no interior-mode scale): hv == 1
+                const bool unit_head = fast && Gen.nf == 1 && p.htab == nullptr && jx < 0;
                 double* Bm = reinterpret_cast<double*>(sB + slot * GB_BYTES + gi * Cfg::B_BYTES);
                 double* Bt = Bm + Cfg::BMAIN;
                 // wide ranks build the item in two chunks of k4-steps (registers)
@@ -474,7 +487,6 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     double u[SPC][NB];
-                    double ut[SPC];
                     bool hsel[SPC];
                     if (fast && P > 0) {
 #pragma unroll
@@ -488,8 +500,6 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                             for (int nb = 0; nb < NB; ++nb)
                                 u[ss][nb] = (valid && nb * 8 + g < C) ? lds_f64(srow + (nb * 8 + g) * 8) : 0.0;
-                            ut[ss] = (TAIL > 0 && valid && g < TAIL && 8 * NB + g < C) ? lds_f64(srow + (8 * NB + g) * 8)
-                                                                                   : 0.0;
                         }
                     } else if (fast) {
 #pragma unroll
@@ -503,7 +513,6 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
 #pragma unroll
                             for (int nb = 0; nb < NB; ++nb)
                                 u[ss][nb] = (valid && nb * 8 + g < C) ? __ldg(row + nb * 8 + g) : 0.0;
-                            ut[ss] = (TAIL > 0 && valid && g < TAIL && 8 * NB + g < C) ? __ldg(row + 8 * NB + g) : 0.0;
                         }
                     } else {
                         // small fastest radix (< 32 rows): full product per entry
@@ -523,36 +532,72 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                                 }
                                 u[ss][nb] = v;
                             }
-                            ut[ss] = 0.0;
-                            if (TAIL > 0) {
-                                const int c = 8 * NB + g;
-                                if (valid && g < TAIL && c < C) {
-                                    ut[ss] = krp_value(Gen, kidx, c);
-                                    if (jx >= 0) ut[ss] *= krp_value(p.sgen, jx, c);
+                        }
+                    }
+                    constexpr int TE = SPC * 4 * (TAIL > 0 ? TAIL : 1);  // tail entries of this chunk
+                    constexpr int TRND = (TE + 31) / 32;
+                    double tv[TRND];
+                    if (TAIL > 0 && !kExpNoTailBuild) {
+                        const int tcn = 8 * NB + tg;
+#pragma unroll
+                        for (int rd = 0; rd < TRND; ++rd) {
+                            const int x = rd * 32 + lane;
+                            const int xs = x / (4 * (TAIL > 0 ? TAIL : 1)), xt = (x / (TAIL > 0 ? TAIL : 1)) & 3;
+                            double val = 0.0;
+                            if (x < TE && tcn < C) {
+                                const int kr = kperm<KMAJ>(ch * SPC + xs, xt);
+                                const long long kidx = kbase + kr;
+                                if (kidx < kext) {
+                                    if (fast) {
+                                        int r = r0 + kr;
+                                        const bool hs = r >= e0;
+                                        if (hs) r -= static_cast<int>(e0);
+                                        const double uv = P > 0 ? lds_f64(sU0a + static_cast<uint32_t>(r * P + tcn) * 8u)
+                                                                : __ldg(U0 + r * ldu + tcn);
+                                        val = uv * (hs ? ht[1] : ht[0]);
+                                    } else {
+                                        val = krp_value(Gen, kidx, tcn);
+                                        if (jx >= 0) val *= krp_value(p.sgen, jx, tcn);
+                                    }
                                 }
                             }
+                            tv[rd] = val;
                         }
                     }
                     if (ch == 0) {
                         if (bw == 0 && lane == 0 && gs == lo) stamp(kTrBuildLoaded);
                         mbar_wait_a(empty_a + 8 * slot, cur.ph ^ 1u);
                     }
+                    if (unit_head) {
+                        // a single-factor B tile (no head partial): the rows as they are
 #pragma unroll
-                    for (int sp = 0; sp < SPC / 2; ++sp) {
-                        const int s2 = ch * SPC / 2 + sp;
+                        for (int sp = 0; sp < SPC / 2; ++sp) {
+                            const int s2 = ch * SPC / 2 + sp;
 #pragma unroll
-                        for (int nb = 0; nb < NB; ++nb) {
-                            double2 v;
-                            v.x = u[2 * sp][nb] * (hsel[2 * sp] ? hv[1][nb] : hv[0][nb]);
-                            v.y = u[2 * sp + 1][nb] * (hsel[2 * sp + 1] ? hv[1][nb] : hv[0][nb]);
-                            *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                            for (int nb = 0; nb < NB; ++nb) {
+                                double2 v;
+                                v.x = u[2 * sp][nb];
+                                v.y = u[2 * sp + 1][nb];
+                                *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int sp = 0; sp < SPC / 2; ++sp) {
+                            const int s2 = ch * SPC / 2 + sp;
+#pragma unroll
+                            for (int nb = 0; nb < NB; ++nb) {
+                                double2 v;
+                                v.x = u[2 * sp][nb] * (hsel[2 * sp] ? hv[1][nb] : hv[0][nb]);
+                                v.y = u[2 * sp + 1][nb] * (hsel[2 * sp + 1] ? hv[1][nb] : hv[0][nb]);
+                                *reinterpret_cast<double2*>(Bm + (((s2 * NB + nb) * 32 + lane) << 1)) = v;
+                            }
                         }
                     }
-                    if (TAIL > 0 && g < TAIL) {
+                    if (TAIL > 0 && !kExpNoTailBuild) {
 #pragma unroll
-                        for (int ss = 0; ss < SPC; ++ss)
-                            Bt[((ch * SPC + ss) * 4 + t) * (TAIL > 0 ? TAIL : 1) + g] =
-                                ut[ss] * (hsel[ss] ? ht[1] : ht[0]);
+                        for (int rd = 0; rd < TRND; ++rd)
+                            if (rd * 32 + lane < TE) Bt[ch * TE + rd * 32 + lane] = tv[rd];
                     }
                 }
                 __syncwarp();
@@ -661,7 +706,11 @@ __global__ void __launch_bounds__(tc_threads(RB), 1)
                 for (int nb = 0; nb < NB; ++nb)
                     dmma_8x8x4(acc[rb][nb][0], acc[rb][nb][1], f.a[sub][rb], sub ? f.bv[nb].y : f.bv[nb].x);
             }
+#ifndef DMTK_EXP_NO_TAIL_FMA
             if (TAIL > 0) {
+#else
+            if (TAIL > 0 && sub > 7) {  // timing experiment: tail FMAs compiled out (wrong results)
+#endif
 #pragma unroll
                 for (int rb = 0; rb < RB; ++rb) {
 #pragma unroll
