@@ -28,6 +28,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <execinfo.h>
 #include <nccl.h>
 
 #include "../../include/dmtk_gpu.h"
@@ -100,6 +101,24 @@ static long long prod(const std::vector<long long>& d, int a, int b) {  // prod 
 // --------------------------------------------------------- device buffers
 // cudaMalloc with the request and the device's free memory in the error text
 static void dev_alloc(void** p, size_t bytes) {
+    if (bytes > (size_t{1} << 42)) {
+        // no buffer of this library is terabytes: a corrupted size. Report
+        // where it came from (library offsets, for addr2line / nm).
+        void* frames[24];
+        const int nfr = backtrace(frames, 24);
+        std::string where;
+        for (int i = 0; i < nfr; ++i) {
+            Dl_info info;
+            char buf[64];
+            if (dladdr(frames[i], &info) && info.dli_fbase) {
+                std::snprintf(buf, sizeof buf, " +0x%zx", static_cast<size_t>(static_cast<char*>(frames[i]) -
+                                                                               static_cast<char*>(info.dli_fbase)));
+                where += buf;
+                if (info.dli_sname) where += std::string("(") + info.dli_sname + ")";
+            }
+        }
+        fail(DMTK_GPU_ERUNTIME, "internal error: device allocation of " + std::to_string(bytes) + " bytes requested at" + where);
+    }
     cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 8));
     if (e == cudaSuccess) return;
     cudaGetLastError();
@@ -874,7 +893,51 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         launch_mttkrp_generic(X, mp.L, mp.I, mp.R, C, kl, kr, mp.jchunk, mp.n_jc, ctx.ws.p, s);
         check_launch("mttkrp_generic");
     } else {
-        mp.tc.bgen = bgen;
+        // A small B side is materialised completely (the KRP of all its
+        // factors, a few MB that stay in L2) and handed to the builders as ONE
+        // factor: its rows are copied into the B tile as they are. The
+        // builders' head multiplies are FP64 DMULs on the pipe the consumers'
+        // DMMAs saturate, and cost 5-10% of a mode where every entry needs one
+        // (measured: 64^5 C=32, 1000^3 C=50); the table costs one more
+        // krp_level launch per call, so it must be small beside the tensor
+        // (200^3: a 5 MB table for a 64 MB tensor cost 2-3 us of a 25 us call).
+        // Larger B sides keep the head table (all factors but the fastest)
+        // and one multiply per entry.
+        KrpGen bg = bgen;
+        static const long long bfull_bytes = [] {
+            const char* e = std::getenv("DMTK_GPU_BFULL_MB");
+            return (e ? std::atoll(e) : 80) << 20;  // 64^5 C=32: the 67 MB three-factor table still pays (+5%)
+        }();
+        bool bfull = false;
+        if (bg.nf >= 2 && bg.ldu == C) {
+            long long tot = 1;
+            bool small = true;
+            for (int f = 0; f < bg.nf; ++f) {
+                tot *= bg.ext[f];
+                if (tot * C * 8 > bfull_bytes || tot * C * 8 > t.ptotal * 8 / 32) {
+                    small = false;
+                    break;
+                }
+            }
+            if (small && tot >= mp.tc.BK) {
+                std::vector<const double*> in;
+                std::vector<long long> rows;
+                for (int f = bg.nf - 1; f >= 0; --f) {  // slowest first: row index = the natural compound index
+                    in.push_back(bg.U[f]);
+                    rows.push_back(bg.ext[f]);
+                }
+                ctx.htab.ensure(static_cast<size_t>(tot * C));
+                krp_materialize(in, rows, C, ctx.htab.p, ctx.scratch2, s);
+                bg = KrpGen{};
+                bg.nf = 1;
+                bg.ldu = C;
+                bg.U[0] = ctx.htab.p;
+                bg.ext[0] = tot;
+                bg.stride[0] = 1;
+                bfull = true;
+            }
+        }
+        mp.tc.bgen = bg;
         mp.tc.sgen = sgen;
         mp.tc.ws = ctx.ws.p;
         // small fastest factor: stage it in shared memory (builders read LDS)
@@ -882,9 +945,9 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         mp.tc.u0_pitch = 0;
         {
             const int P = C + ((6 - C % 4) % 4);
-            const long long bytes = bgen.ext[0] * P * 8;
+            const long long bytes = bg.ext[0] * P * 8;
             const int padded = static_cast<int>((bytes + 127) / 128 * 128);
-            if (bgen.ext[0] >= mp.tc.BK && bgen.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
+            if (bg.ext[0] >= mp.tc.BK && bg.ldu > 0 && bytes <= 48 * 1024 && mp.tc.smem + padded <= 227 * 1024 &&
                 !std::getenv("DMTK_GPU_NO_U0_SMEM")) {
                 mp.tc.u0_pitch = P;
                 mp.tc.smem += padded;
@@ -894,7 +957,9 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
         // krp.cpp:53-88), materialised once so a builder's head is one row load
         mp.tc.htab = nullptr;
         mp.tc.hrows = 0;
-        if (bgen.nf == 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu == C) {
+        if (bfull) {
+            // (the complete table above: no heads)
+        } else if (bgen.nf == 2 && bgen.ext[0] >= mp.tc.BK && bgen.ldu == C) {
             // one slower factor: the head table is that factor itself (no copy)
             mp.tc.htab = bgen.U[1];
             mp.tc.hrows = bgen.ext[1];
@@ -1100,7 +1165,9 @@ static void tune_load_locked() {
         std::string dir(info.dli_fname);
         const size_t slash = dir.rfind('/');
         dir = slash == std::string::npos ? std::string(".") : dir.substr(0, slash);
-        tune_read((dir + "/tune_b200.txt").c_str(), g_tune_pkg, &g_tune_pkg_sms);
+        // (DMTK_GPU_NO_TUNE_TABLE: ignore the packaged table -- tools/make_tune_table.py re-measures it)
+        if (!std::getenv("DMTK_GPU_NO_TUNE_TABLE"))
+            tune_read((dir + "/tune_b200.txt").c_str(), g_tune_pkg, &g_tune_pkg_sms);
     }
     if (const char* path = tune_cache_path()) tune_read(path, g_tune, nullptr);
 }
@@ -2747,7 +2814,11 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
                 als_upd(n, M.p);
         };
         // Dimension tree (dmtk_gpu.h, dimtree): halves [0, h) and [h, N)
-        const bool tree = cfg->dimtree != 0 && N >= 3;
+        // (a packed symmetric tensor runs its own tree below; its pdims have one
+        // entry less than dims, so none of the generic tree sizing applies to it:
+        // it read one element past pdims and, now and then, sized Pbuf from
+        // heap garbage)
+        const bool tree = !t->sym01 && cfg->dimtree != 0 && N >= 3;
         int hsplit = 0;
         DevBuf Pbuf;
         if (tree) {

@@ -44,7 +44,7 @@ def shard_extents(extent, world):
 def main():
     fd, path = tempfile.mkstemp(suffix=".txt")
     os.close(fd)
-    env = dict(os.environ, DMTK_GPU_AUTOTUNE="1", DMTK_GPU_TUNE_CACHE=path)
+    env = dict(os.environ, DMTK_GPU_AUTOTUNE="1", DMTK_GPU_TUNE_CACHE=path, DMTK_GPU_NO_TUNE_TABLE="1")
     shapes = []
     for dims, C in CONFIGS:
         for world in (1, 2, 4, 8):
