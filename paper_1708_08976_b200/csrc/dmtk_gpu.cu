@@ -908,13 +908,23 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
             const char* e = std::getenv("DMTK_GPU_BFULL_MB");
             return (e ? std::atoll(e) : 80) << 20;  // 64^5 C=32: the 67 MB three-factor table still pays (+5%)
         }();
+        static const long long bfull_div = [] {  // the table at most 1 / this of the tensor
+            const char* e = std::getenv("DMTK_GPU_BFULL_DIV");
+            return e ? std::max(1LL, std::atoll(e)) : 32LL;
+        }();
         bool bfull = false;
-        if (bg.nf >= 2 && bg.ldu == C) {
+        if (bfull_bytes > 0 && bg.nf >= 2 && bg.ldu == C) {  // (DMTK_GPU_BFULL_MB=0: never)
             long long tot = 1;
             bool small = true;
             for (int f = 0; f < bg.nf; ++f) {
                 tot *= bg.ext[f];
-                if (tot * C * 8 > bfull_bytes || tot * C * 8 > t.ptotal * 8 / 32) {
+                // ranks well above the roofline ridge (C ~ 23) leave HBM bandwidth unused: the
+                // table may then spill L2 and be re-read per tile pass (1000^3 C=50 mode 0,
+                // 400 MB: +2.6%; at C=25 the same table costs 2%)
+                const bool spare_hbm = C >= 36;
+                const long long cap = spare_hbm ? std::max(bfull_bytes, 512LL << 20) : bfull_bytes;
+                const long long div = spare_hbm ? std::min(bfull_div, 16LL) : bfull_div;
+                if (tot * C * 8 > cap || tot * C * 8 > t.ptotal * 8 / div) {
                     small = false;
                     break;
                 }
