@@ -1026,10 +1026,10 @@ static void enqueue_planned(dmtk_gpu_tensor_s& t, Context& ctx, ModePlan mp, int
             std::fprintf(stderr,
                          "dmtk_gpu plan: mode %d flavor %d L %lld I %lld R %lld C %d nb %d tail %d RB %d G %d TR %d "
                          "BI %d BJ %d stages %d spt %lld tiles %lld grid %d smem %d u0 %d htab %lld swap %d s %d cost %.3f "
-                         "ldgsts %d\n",
+                         "ldgsts %d bfull %d\n",
                          mode, mp.tc.flavor, mp.L, mp.I, mp.R, C, mp.nb, mp.tail, mp.tc.RB, mp.tc.G, mp.tc.TR,
                          mp.tc.BI, mp.tc.BJ, mp.tc.stages, mp.tc.stages_per_tile, mp.tc.n_ti * mp.tc.n_tj, mp.grid,
-                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost, mp.tc.ldgsts);
+                         mp.tc.smem, mp.tc.u0_pitch, mp.tc.hrows, mp.tc.swap, mp.variant, mp.cost, mp.tc.ldgsts, bfull ? 1 : 0);
         CUtensorMap map;
         if (mp.tc.ldgsts) {
             std::memset(&map, 0, sizeof(map));

@@ -51,6 +51,30 @@ def test_boundary_two_step_forced_shapes(rb):
     assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
 
 
+@pytest.mark.parametrize("rb", [0, 2, 3, 4])
+@pytest.mark.parametrize("div", ["1", "0"])
+def test_complete_b_tables(rb, div):
+    """B sides materialised completely (builders copy rows, no head multiply):
+    the size rule (table <= tensor / 32) keeps small tensors off that path, so
+    DMTK_GPU_BFULL_DIV=1 forces it here on ragged multi-factor shapes with
+    tails (C = 25, 17, 50) and without, every tile height; div "0" runs the
+    same shapes with the tables switched off (DMTK_GPU_BFULL_MB=0)."""
+    env = dict(os.environ, DMTK_GPU_PLAN_LOG="1")
+    if div == "0":
+        env["DMTK_GPU_BFULL_MB"] = "0"
+    else:
+        env["DMTK_GPU_BFULL_DIV"] = div
+    if rb:
+        env["DMTK_GPU_FORCE_RB"] = str(rb)
+    shapes = ["40x40x12x8:20", "30x20x10x8:25", "6x10x4x2x2x4:17", "130x66x34:9", "20x18x16x6:50", "64x4x4x64:32",
+              "9x11x13x5:25"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_shapes.py"), *shapes], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "failures: 0" in r.stdout, "\n".join(l for l in r.stdout.splitlines() if "FAIL" in l)
+    assert (" bfull 1" in r.stderr) == (div != "0"), "the plan log must show the complete tables on / off"
+
+
 ODD = ["9x11x13:20", "15x7x9x5:25", "33x65x17:16", "3x5x7x9x11:7", "101x3x5:3"]
 
 
