@@ -42,7 +42,11 @@ __host__ __device__ constexpr int tc_bm(int rb) { return kConsumerWarps * 8 * rb
 // Warp roles: producer, three builders, eight consumers (see mttkrp_tc.cuh).
 // (A setmaxnreg rebalance toward the consumers was measured to add spills,
 // not remove them: ptxas keeps values live across the role split.)
-__host__ __device__ constexpr int tc_builders(int) { return 3; }
+#ifndef DMTK_TC_BUILDERS
+#define DMTK_TC_BUILDERS 3  // (build macro; 2 builders measured 1-5% slower, and 11 warps get the same 168
+                            // registers per thread as 12: the register file is allocated per four warps)
+#endif
+__host__ __device__ constexpr int tc_builders(int) { return DMTK_TC_BUILDERS; }
 __host__ __device__ constexpr int tc_threads(int rb) { return (kConsumerWarps + tc_builders(rb) + 1) * 32; }
 constexpr int kProducerWarp = 0;
 constexpr int kFirstBuilderWarp = 1;
