@@ -2725,7 +2725,8 @@ static void cp_als_run(dmtk_gpu_tensor t, const dmtk_gpu_als_config* cfg, const 
         M.ensure(static_cast<size_t>(maxrows * C));
         const int iters = cfg->max_iters;
         const int fit_slots = std::max(iters, 1) + 1;
-        const long long solve_doubles = wide ? wide_scratch_doubles(C, maxrows) + CM : 3 * 64 * 64 + 64;
+        const long long solve_doubles =
+            wide ? wide_scratch_doubles(C, maxrows) + CM : 3 * 64 * 64 + 64 + als_fused_scratch_doubles();
         aux.ensure(static_cast<size_t>(CM + CM * CM + N * C * C + 1 + 4 * fit_slots + solve_doubles));
         double* lam = aux.p;
         double* H = lam + CM;

@@ -853,6 +853,194 @@ __global__ void __launch_bounds__(1024) als_solve_gj_kernel(const double* __rest
     if (tid == 0) flag[0] = 1;
 }
 
+// The whole factor update in two launches (ranks <= 32; DMTK_GPU_ALS_FUSED=0 keeps the
+// four-launch chain solve / apply / normalise / Gram):
+//  1. als_solve_apply_kernel: EVERY CTA forms the Hadamard product and inverts it
+//     (the same Gauss-Jordan steps and Jacobi fallback as als_solve_gj_kernel -- the
+//     serial part is not made longer by running it in up to 148 copies), then takes
+//     row blocks of U = M H^-1 (unnormalised) and accumulates the Gram of its own rows;
+//  2. als_scale_gram_kernel: the column norms are the square roots of the summed Gram
+//     diagonals, every CTA scales its rows, CTA 0 writes lambda and the Gram of the
+//     normalised factor, G(i, j) / (lambda_i lambda_j).
+// Partial Grams are summed over the CTAs in a fixed order (the grid depends only on the
+// row count), products commute exactly, so G is symmetric to the bit and the update is
+// deterministic.
+constexpr int kAlsFusedThreads = 512;
+constexpr int kAlsFusedCtas = 148;
+long long als_fused_scratch_doubles() { return static_cast<long long>(kAlsFusedCtas) * 32 * 32; }
+
+__global__ void __launch_bounds__(kAlsFusedThreads) als_solve_apply_kernel(
+    const double* __restrict__ grams, int nmodes, int skip, int n, double* __restrict__ Hout, double* __restrict__ Hinv,
+    const double* __restrict__ M, long long rows, double* __restrict__ U, double* __restrict__ part,
+    int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int LDA = 33;
+    __shared__ double A[2][32 * LDA];
+    __shared__ double sHi[32 * 32];
+    __shared__ double sU[kAlsFusedThreads];
+    __shared__ double s_tr;
+    __shared__ double s_gain[32];
+    const int tid = threadIdx.x;
+    const int nn = n * n;
+    for (int e = tid; e < nn; e += blockDim.x) {
+        double h = 1.0;
+        for (int k = 0; k < nmodes; ++k)
+            if (k != skip) h *= grams[static_cast<long long>(k) * nn + e];
+        Hout[e] = h;  // (every CTA writes the same values)
+        const int i = e / n, j = e - (e / n) * n;
+        A[0][i * LDA + j] = h;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        double v = tid < n ? A[0][tid * LDA + tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tid == 0) s_tr = v;
+    }
+    __syncthreads();
+    const double tol = 1e-12 * s_tr;
+    const bool own = nn <= static_cast<int>(blockDim.x);
+    const int oi = tid / n, oj = tid - (tid / n) * n;
+    bool singular = false;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        const double* a = A[k & 1];
+        double* b = A[(k + 1) & 1];
+        const double p = a[k * LDA + k];
+        if (p <= tol) {  // uniform across the CTA (and across the CTAs: the same arithmetic)
+            singular = true;
+            break;
+        }
+        const double r = 1.0 / p;
+        for (int e = tid; e < nn; e += blockDim.x) {
+            const int i = own ? oi : e / n, j = own ? oj : e - (e / n) * n;
+            double v;
+            if (i == k)
+                v = j == k ? r : a[k * LDA + j] * r;
+            else if (j == k)
+                v = -a[i * LDA + k] * r;
+            else
+                v = fma(-a[i * LDA + k] * r, a[k * LDA + j], a[i * LDA + j]);
+            b[i * LDA + j] = v;
+        }
+        __syncthreads();
+    }
+    if (singular) {
+        __threadfence();  // this CTA's Hout is read back from global memory below
+        __syncthreads();
+        jacobi_pinv_cta<LDA>(Hout, n, A[0], A[1], s_gain, Hinv);  // writes Hinv (global)
+        __threadfence();
+        __syncthreads();
+        for (int e = tid; e < nn; e += blockDim.x) sHi[e] = Hinv[e];
+    } else {
+        const double* a = A[n & 1];
+        for (int e = tid; e < nn; e += blockDim.x) {
+            const int i = e / n, j = e - (e / n) * n;
+            const double v = 0.5 * (a[i * LDA + j] + a[j * LDA + i]);  // symmetric to the last bit
+            sHi[e] = v;
+            Hinv[e] = v;
+        }
+    }
+    if (tid == 0 && blockIdx.x == 0) flag[0] = 1;
+    __syncthreads();
+    // rows of U = M H^-1 in blocks of RPB, and the Gram of this CTA's rows
+    const int RPB = kAlsFusedThreads / n;
+    const int lr = tid / n, lc = tid - lr * n;
+    double gacc[2] = {0.0, 0.0};  // entries tid and tid + 512 (n <= 32: at most two per thread)
+    for (long long blk = blockIdx.x; blk * RPB < rows; blk += gridDim.x) {
+        const long long r = blk * RPB + lr;
+        if (lr < RPB) {
+            double u = 0.0;
+            if (r < rows) {
+                const double* mrow = M + r * n;
+                double t[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int k0 = 0; k0 < n; k0 += 8) {
+                    double m[8], h[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = k0 + q;
+                        m[q] = k < n ? __ldg(mrow + k) : 0.0;
+                        h[q] = k < n ? sHi[k * n + lc] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) t[q & 3] = fma(m[q], h[q], t[q & 3]);
+                }
+                u = (t[0] + t[1]) + (t[2] + t[3]);
+                U[r * n + lc] = u;
+            }
+            sU[lr * n + lc] = u;  // (rows past the end: zeros)
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const int e = tid + w * kAlsFusedThreads;
+            if (e < nn) {
+                const int i = e / n, j = e - (e / n) * n;
+                double q4[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int rr = 0; rr < RPB; ++rr) q4[rr & 3] = fma(sU[rr * n + i], sU[rr * n + j], q4[rr & 3]);
+                gacc[w] += (q4[0] + q4[1]) + (q4[2] + q4[3]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+        const int e = tid + w * kAlsFusedThreads;
+        if (e < nn) part[static_cast<long long>(blockIdx.x) * nn + e] = gacc[w];
+    }
+}
+
+__global__ void __launch_bounds__(kAlsFusedThreads) als_scale_gram_kernel(double* __restrict__ U, long long rows, int n,
+                                                                          const double* __restrict__ part, int nb,
+                                                                          double* __restrict__ lambda,
+                                                                          double* __restrict__ G) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double s_part[kAlsFusedThreads];
+    __shared__ double s_inv[32];
+    const int tid = threadIdx.x;
+    const int nn = n * n;
+    // column sums of squares = the Gram diagonals summed over the nb partials:
+    // thread (q, c) takes partials q, q + Q, ... in four chains, then a fixed fold over q
+    const int Q = kAlsFusedThreads / n;
+    const int q = tid / n, c = tid - q * n;
+    double s = 0.0;
+    if (q < Q) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        int k = 0;
+        for (int b = q; b < nb; b += Q, ++k) t[k & 3] += part[static_cast<long long>(b) * nn + c * n + c];
+        s = (t[0] + t[1]) + (t[2] + t[3]);
+    }
+    s_part[tid] = s;
+    __syncthreads();
+    if (tid < n) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < Q; ++k) t[k & 3] += s_part[k * n + tid];
+        const double nrm = sqrt((t[0] + t[1]) + (t[2] + t[3]));
+        s_inv[tid] = nrm > 0.0 ? 1.0 / nrm : 1.0;  // (a zero column stays as it is, cp_als.cpp:101-118)
+        if (blockIdx.x == 0) lambda[tid] = nrm;
+    }
+    __syncthreads();
+    const int RPB = kAlsFusedThreads / n;
+    const int lr = tid / n, lc = tid - lr * n;
+    if (lr < RPB) {
+        const double inv = s_inv[lc];
+        for (long long blk = blockIdx.x; blk * RPB < rows; blk += gridDim.x) {
+            const long long r = blk * RPB + lr;
+            if (r < rows) U[r * n + lc] *= inv;
+        }
+    }
+    if (blockIdx.x == 0) {
+        for (int e = tid; e < nn; e += blockDim.x) {
+            const int i = e / n, j = e - (e / n) * n;
+            double t[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int b = 0; b < nb; ++b) t[b & 3] += part[static_cast<long long>(b) * nn + e];
+            G[e] = ((t[0] + t[1]) + (t[2] + t[3])) * (s_inv[i] * s_inv[j]);
+        }
+    }
+}
+
 // U = M H^-1, one output element per thread (H^-1 staged in shared memory).
 __global__ void apply_inverse_kernel(const double* __restrict__ Hinv, int n, const double* __restrict__ M,
                                      long long rows, double* __restrict__ U, const int* __restrict__ flag) {
@@ -1446,6 +1634,23 @@ int launch_als_update(const double* grams, int nmodes, int C, int skip, double* 
     // (a single-CTA fusion of these steps was measured slower: one CTA's
     // latency chains cost more than the launches it saves)
     static const bool exact = std::getenv("DMTK_GPU_ALS_EXACT_SOLVE") != nullptr;
+    static const bool chol_env = std::getenv("DMTK_GPU_ALS_CHOL_INVERSE") != nullptr;
+    static const bool fused = [] {
+        const char* e = std::getenv("DMTK_GPU_ALS_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (!exact && !chol_env && fused && C <= 32 && !solve_only) {
+        // solve + apply + partial Grams, then norms + scaling + Gram: two launches
+        double* Hinv = scratch;
+        double* part = scratch + 3 * 64 * 64 + 64;  // (als_fused_scratch_doubles() after the solve scratch)
+        const int RPB = kAlsFusedThreads / C;
+        const int nb = static_cast<int>(std::min<long long>(kAlsFusedCtas, (rows + RPB - 1) / RPB));
+        launch_pdl(als_solve_apply_kernel, dim3(nb), dim3(kAlsFusedThreads), 0, s, grams, nmodes, skip, C, H, Hinv, M, rows,
+                   U, part, flag);
+        launch_pdl(als_scale_gram_kernel, dim3(nb), dim3(kAlsFusedThreads), 0, s, U, rows, C, static_cast<const double*>(part),
+                   nb, lambda, Gn);
+        return 2;
+    }
     if (!exact && C <= 32) {  // Hadamard + Cholesky + H^-1 in one CTA, then U = M H^-1
         double* Hinv = scratch;
         double* V = scratch + 64 * 64;

@@ -118,6 +118,7 @@ void launch_fit_from_inner(const double* lambda, int C, const double* Hlast, con
                            const double* normx, const double* inner, double* out, cudaStream_t s);
 // One ALS factor update (Hadamard of cached Grams, solve through H^-1,
 // normalise, new Gram). Returns the launch count.
+long long als_fused_scratch_doubles();  // partial-Gram scratch after the 3 * 64 * 64 + 64 solve scratch
 int launch_als_update(const double* grams, int nmodes, int C, int skip, double* H, const double* M, long long rows,
                       double* U, double* lambda, double* Gn, double* scratch, int* flag, cudaStream_t s,
                       bool solve_only = false);
