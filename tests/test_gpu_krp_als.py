@@ -5,6 +5,7 @@ krp.hpp:19-32) and the reference's KrpStats counts (test_krp.cpp:108-155).
 CP-ALS: reference test_cpals.cpp cases, plus fits within 1e-9 of the
 reference after the same number of iterations (BASELINE.json north_star).
 """
+import os
 import numpy as np
 import pytest
 
@@ -12,6 +13,7 @@ import paper_1708_08976_b200 as dg
 from paper_1708_08976_b200 import AlsConfig, MttkrpAlgo as A
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def inputs(oracle, dims, cols, seed):
@@ -76,7 +78,10 @@ def cp(x, dims, rank, iters, seed, tol=0.0, algo=A.automatic, tree=False):
 
 
 @pytest.mark.parametrize("dims,rank,iters", [((6, 5, 4), 3, 6), ((7, 6, 5), 3, 8), ((8, 9, 10), 4, 40),
-                                             ((12, 10, 8, 6), 5, 10), ((40, 40, 12, 8), 20, 25)])
+                                             ((12, 10, 8, 6), 5, 10), ((40, 40, 12, 8), 20, 25),
+                                             # ranks above 22: two Gram / inverse entries per thread of the
+                                             # two-launch factor update; 4000 rows: several row blocks per CTA
+                                             ((30, 28, 26), 32, 8), ((4000, 6, 5), 27, 6), ((33, 9, 7, 5), 23, 8)])
 def test_cp_als_fits_match_reference(ref, oracle, dims, rank, iters):
     x = oracle.gen_tensor(dims, 31)
     got = cp(x, dims, rank, iters, 7)
@@ -106,6 +111,28 @@ def test_cp_als_dimension_tree_matches_reference(ref, oracle, dims, rank, iters)
         assert np.allclose(np.linalg.norm(u, axis=0), 1.0, rtol=1e-12, atol=0)
     again = cp(x, dims, rank, iters, 7, tree=True)  # deterministic
     assert [r.fit.fit for r in again.trace.iters] == list(f_got)
+
+
+def test_cp_als_four_launch_update_chain_matches_reference(ref, oracle):
+    """DMTK_GPU_ALS_FUSED=0 (read once per process, hence the subprocess): the
+    solve / apply / normalise / Gram chain gives the reference's fits too."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path[:0] = [%r, %r]\n"
+        "import paper_1708_08976_b200 as dg\n"
+        "from oracle_bindings import Oracle, Ref\n"
+        "o, r = Oracle(), Ref()\n"
+        "for dims, rank, iters in (((12, 10, 8, 6), 5, 10), ((30, 28, 26), 32, 6)):\n"
+        "    x = o.gen_tensor(dims, 31)\n"
+        "    got = dg.cp_als(dg.DenseTensor(dims, x), dg.AlsConfig(rank=rank, max_iters=iters, tol=0.0, seed=7))\n"
+        "    want = r.cp_als(x, dims, rank, iters, tol=0.0, seed=7)\n"
+        "    f = np.array([it.fit.fit for it in got.trace.iters])\n"
+        "    assert np.max(np.abs(f - want['fits'])) <= 1e-9, (dims, f, want['fits'])\n"
+        "print('ok')\n" % (ROOT, os.path.join(ROOT, "tests")))
+    env = dict(os.environ, DMTK_GPU_ALS_FUSED="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-3000:]
 
 
 def test_cp_als_monotone_and_deterministic(oracle):
